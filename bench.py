@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark of the fused B200 uplink receive path (BASELINE.json metric:
+OFDM symbols/s at 64 antennas x FFT-1024, 16-QAM, 1 pilot + 10 data
+symbols per frame; frame-sharded over 1/2/4/8 GPUs, weak scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = one fused launch over F frames per GPU resident in HBM (inputs
+6.3 GB/GPU >> 126 MB L2, so no L2 flush is needed between steps).
+Prints one JSON line on rank 0.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (N antennas, M, CP, QAM, D data symbols, frames per GPU)
+    "C1": (8, 64, 16, 4, 10, 65536),
+    "C2": (16, 256, 32, 16, 10, 1000),
+    "C3": (64, 1024, 72, 16, 10, 1024),
+    "C4": (256, 2048, 256, 64, 10, 64),
+}
+METRIC = "OFDM symbols/s & per-stage µs/symbol at 64 ant × FFT 1024, 1/2/4/8 B200"
+DISTINCT = 16  # distinct synthetic frames, tiled on the device
+
+
+def frame_bytes(n, m, qam, d):
+    """Algorithmic HBM bytes per frame: rx samples of the
+    1+D symbols without CP, H written once, s_hat, bits as u8."""
+    b = int(math.log2(qam))
+    return 8 * n * m * (1 + d) + 8 * n * m + 8 * m * d + b * m * d
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_inputs(cfg_name, seed_base=0):
+    from paper_1901_07499_b200 import synth
+    from paper_1901_07499_b200.waveform import OfdmConfig
+
+    n, m, cp, qam, d, _ = CONFIGS[cfg_name]
+    cfg = OfdmConfig(m, cp, n, qam_order=qam)
+    rx, bits, s0 = synth.synth_batch(cfg, d, range(seed_base, seed_base + DISTINCT), snr_db=10.0)
+    return cfg, rx, bits, s0
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines
+# ---------------------------------------------------------------------------
+
+def cpu_port_baseline(cfg_name, rx_host, budget_s=10.0):
+    """The oracle port (numpy restatement of the reference path), 1 thread,
+    on a bounded sample of the same frames."""
+    from oracle import ofdm_oracle as orc
+
+    n, m, cp, qam, d, _ = CONFIGS[cfg_name]
+    x = rx_host.astype(np.complex128)
+    frames = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        orc.receive_frame(x[frames % x.shape[0]], 0, m, cp, d, qam)
+        frames += 1
+    dt = time.perf_counter() - t0
+    return {"value": frames * (1 + d) / dt, "unit": "symbols/s", "cores": 1, "kind": "port",
+            "sample": f"{frames} {cfg_name} frames ({frames * (1 + d)} OFDM symbols), oracle/ofdm_oracle.py "
+                      f"receive_frame (numpy radix-2 as reference numpy_backend), {dt:.1f} s"}
+
+
+def reference_importable():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "ofdmrx")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        return True
+    return False
+
+
+def run_reference_arm(args, cfg_name, world, rank):
+    """--impl reference: the reference's own CPU implementation of the path
+    (baseline/_ref = unmodified ofdmrx, run_ring_pipeline) on this host's
+    cores; falls back to the oracle port when the install is absent."""
+    n, m, cp, qam, d, _ = CONFIGS[cfg_name]
+    if rank != 0:
+        return None
+    ncores = len(os.sched_getaffinity(0))
+    from paper_1901_07499_b200 import synth
+    from paper_1901_07499_b200.waveform import OfdmConfig
+
+    cfg = OfdmConfig(m, cp, n, qam_order=qam)
+    caps = [synth.synth_capture(cfg, d, s, 10.0) for s in range(4)]
+    line = {"metric": METRIC, "unit": "symbols/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic (reference TX + flat Rayleigh 10 dB)",
+            "config": {"workload": f"{cfg_name}: {n} ant x FFT {m} (CP {cp}), {qam}-QAM, 1 pilot + {d} data "
+                                   "symbols/frame", "frames_per_step": None}}
+    if not reference_importable():
+        # oracle port (numpy restatement) as the reference CPU implementation
+        from oracle import ofdm_oracle as orc
+
+        def step(nf):
+            for i in range(nf):
+                c = caps[i % len(caps)]
+                orc.receive_frame(c.streams, c.symbol0_offset, m, cp, d, qam)
+        engine_desc, kind, cores = "oracle port (numpy, 1 thread)", "port", 1
+    else:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ofdmrx_numba_cache")
+        from ofdmrx import receiver as rref, waveform as wref
+        from ofdmrx.sync import DetectionResult
+
+        class _Cap:
+            def __init__(self, s):
+                self.streams = s
+
+        rcfg = wref.OfdmConfig(m, cp, n, qam_order=qam)
+        pilot = wref.make_pilot(m)
+        slot_sets = [rref.extract_slots(_Cap(c.streams), DetectionResult(True, 0, c.symbol0_offset, 1.0, ()),
+                                        rcfg, 1 + d) for c in caps]
+        engines = {"sequential": rref.EngineKind("sequential"),
+                   f"data_parallel({ncores})": rref.EngineKind("data_parallel", ncores)}
+        best = None
+        for name, kind_ in engines.items():
+            with rref.make_engine(kind_) as eng:
+                rref.run_ring_pipeline(slot_sets[0], rcfg, eng, pilot=pilot)  # JIT / pool warm-up
+                t0 = time.perf_counter()
+                rref.run_ring_pipeline(slot_sets[1], rcfg, eng, pilot=pilot)
+                dt = time.perf_counter() - t0
+            if best is None or dt < best[1]:
+                best = (name, dt, kind_)
+        from ofdmrx import kernels as kref
+
+        chosen = best[2]
+        eng = rref.make_engine(chosen)
+
+        def step(nf):
+            for i in range(nf):
+                rref.run_ring_pipeline(slot_sets[i % len(slot_sets)], rcfg, eng, pilot=pilot)
+        engine_desc = f"reference ofdmrx run_ring_pipeline, backend={kref.BACKEND}, engine={best[0]} " \
+                      f"(fastest of sequential / data_parallel({ncores}))"
+        kind = "reference"
+        cores = ncores if chosen.variant == "data_parallel" else 1
+    # size each step to ~2 s of CPU work
+    t0 = time.perf_counter()
+    step(1)
+    per_frame = max(time.perf_counter() - t0, 1e-4)
+    nf = max(1, int(2.0 / per_frame))
+    for _ in range(args.warmup):
+        step(nf)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(nf)
+    dt = time.perf_counter() - t0
+    value = args.steps * nf * (1 + d) / dt
+    line.update({"value": value, "ms_per_step": dt / args.steps * 1e3,
+                 "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": cores, "kind": kind,
+                                  "sample": f"{nf} frames/step x {args.steps} steps; {engine_desc}"},
+                 "e2e": {"value": value, "unit": "symbols/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    line["config"]["frames_per_step"] = nf
+    return line
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args, cfg_name, world, rank, local):
+    import torch
+
+    import paper_1901_07499_b200 as P
+    from paper_1901_07499_b200 import frames
+
+    n, m, cp, qam, d, F = CONFIGS[cfg_name]
+    if args.frames:
+        F = args.frames
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg, rx_host, bits_truth, s0 = make_inputs(cfg_name, seed_base=1000 * rank)
+    base = torch.from_numpy(rx_host).to(dev)
+    reps = (F + DISTINCT - 1) // DISTINCT
+    x = base.repeat(reps, 1, 1)[:F].contiguous()
+    del base
+    out = frames.allocate_outputs(F, n, m, d, qam, dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out)
+
+    # correctness spot-check of the benchmarked configuration (bits vs truth)
+    step()
+    torch.cuda.synchronize()
+    ber = float((out.bits[:DISTINCT].cpu().numpy() != bits_truth[: min(DISTINCT, F)]).mean())
+    flags_bad = int((out.flags != 0).sum())
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        time.sleep(0.3)
+        barrier(world)
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_stop = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_stop.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    total_ms = t_start.elapsed_time(t_stop)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    ms_step = allreduce_max(world, total_ms / args.steps)
+    value = world * F * (1 + d) / (ms_step * 1e-3)
+
+    peak, peak_kind = load_peaks()
+    bpf = frame_bytes(n, m, qam, d)
+    achieved = bpf * F / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg_name}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 (cf32 I/O)",
+        "data": "synthetic: reference TX (PN|pilot|data, Gray QAM) through flat Rayleigh at 10 dB; "
+                f"{DISTINCT} distinct frames tiled on device",
+        "config": {"workload": f"{cfg_name}: {n} ant x FFT {m} (CP {cp}), {qam}-QAM, 1 pilot + {d} data symbols/frame",
+                   "frames_per_gpu": F, "global_frames": F * world, "parallelism": f"frame-sharded x{world}",
+                   "input_bytes_per_gpu": int(x.numel() * 8), "l2": "inputs 6.3 GB/GPU > L2, no flush needed"
+                   if x.numel() * 8 > 126e6 else "inputs smaller than L2"},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "bytes_per_frame": bpf, "kernel_ms": kernel_ms},
+        "clocks": clocks.summary(),
+        "check": {"ber_vs_tx": ber, "flagged_frames": flags_bad},
+        "data_symbols_per_s": world * F * d / (ms_step * 1e-3),
+    }
+    if args.e2e_frames > 0:
+        line["e2e"] = run_e2e(args, cfg, x, s0, d, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_port_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds)
+    return line
+
+
+def run_e2e(args, cfg, x_dev, s0, d, world):
+    """Same metric through the public API from pinned host memory: every step
+    copies its frames H2D, runs receive_frames, and reads the bits back."""
+    import torch
+
+    from paper_1901_07499_b200 import frames
+
+    Fe = min(args.e2e_frames, x_dev.shape[0])
+    host = torch.empty((Fe,) + tuple(x_dev.shape[1:]), dtype=torch.complex64, pin_memory=True)
+    host.copy_(x_dev[:Fe].cpu())
+    bits_host = torch.empty((Fe, d * cfg.fft_len * cfg.bits_per_qam_symbol), dtype=torch.uint8, pin_memory=True)
+    rx = frames.StreamingReceiver(cfg, Fe, symbol0_offset=s0, n_data=d) if hasattr(frames, "StreamingReceiver") else None
+
+    def step():
+        if rx is not None:
+            rx.run(host, bits_host)
+        else:
+            out = frames.receive_frames(host, cfg, symbol0_offset=s0, n_data=d, want_h=False)
+            bits_host.copy_(out.bits, non_blocking=True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = allreduce_max(world, a.elapsed_time(b) / args.steps)
+    return {"value": world * Fe * (1 + d) / (ms * 1e-3), "unit": "symbols/s",
+            "h2d_bytes_per_step": int(host.numel() * 8), "d2h_bytes_per_step": int(bits_host.numel()),
+            "frames_per_step": Fe, "ms_per_step": ms,
+            "path": "pinned host -> receive_frames (public API) -> bits to pinned host"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default per config)")
+    ap.add_argument("--e2e-frames", type=int, default=64)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        line = run_reference_arm(args, args.config, world, rank)
+        if line is not None:
+            line["n_gpus"] = world
+            print(json.dumps(line), flush=True)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    line = run_b200(args, args.config, world, rank, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/*
+ * ofdmrx_b200 — C ABI of the B200 (sm_100a) uplink OFDM receive path.
+ *
+ * Drop-in boundary for the reference receiver's hot path
+ * (/root/reference/pkg/src/ofdmrx).  The reference has no native FFI — its
+ * swap points are the Python engine protocol (receiver.py:88-179) and the
+ * kernel-backend protocol (kernels/__init__.py:40-68).  Each entry point below
+ * names the reference interface it replaces; INTEGRATION.md shows the ctypes
+ * binding a maintainer adds to the reference to route those calls here.
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *    complex samples are interleaved float32 (cf32, the .cf32 file layout of
+ *    io_formats.py:18-30), bits are uint8 0/1 (waveform.qam_demap's format).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    stream-ordered and asynchronous: returning OFDMRX_OK means "validated and
+ *    enqueued"; per-frame data errors are reported through `flags`.
+ *  - Subcarrier order of every frequency-domain array is the reference's
+ *    fftshift-ed order (numerics.py:57-64).
+ *  - Return value: 0 = OK, otherwise an ofdmrx_status whose category mirrors
+ *    errors.py (ConfigurationError, ContractError, InputError/FramingError,
+ *    NumericInputError); ofdmrx_last_error() returns the message
+ *    (thread-local).
+ *  - rx buffers must be 8-byte aligned and readable up to the next 16-byte
+ *    boundary past the last sample used (TMA bulk copies move whole 16-byte
+ *    granules; torch/cudaMalloc allocations satisfy this).
+ */
+#ifndef OFDMRX_B200_H_
+#define OFDMRX_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OFDMRX_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define OFDMRX_API __attribute__((visibility("default")))
+#else
+#define OFDMRX_API
+#endif
+
+typedef enum {
+  OFDMRX_OK = 0,
+  OFDMRX_ERR_CONFIG = 1,   /* errors.ConfigurationError (errors.py:10-13) */
+  OFDMRX_ERR_CONTRACT = 2, /* errors.ContractError (errors.py:28-31)      */
+  OFDMRX_ERR_INPUT = 3,    /* errors.FramingError / InputError (34-43)     */
+  OFDMRX_ERR_NUMERIC = 4,  /* errors.NumericInputError (16-19)             */
+  OFDMRX_ERR_CUDA = 5      /* device / launch failure                      */
+} ofdmrx_status;
+
+/* Per-frame flag bits written by the fused / finish kernels (atomic OR). */
+#define OFDMRX_FLAG_NONFINITE 1u /* a non-finite sample reached the FFT: to_freq raises NumericInputError (receiver.py:202-203) */
+#define OFDMRX_FLAG_ERASED 2u    /* some subcarrier weight < eps: CombinedSymbol.erased (receiver.py:234) */
+
+/*
+ * Batch of F captures, each N antenna rows of samples.  Frame f, antenna n,
+ * symbol s (s = 0 pilot, 1..D data) starts at sample
+ *     f*frame_stride + n*row_stride + symbol0_offset + s*(fft_len + cp_len)
+ * and its first cp_len samples are the cyclic prefix (never read).
+ * This is extract_slots (receiver.py:274-291) + cp_drop (186-193) expressed as
+ * strides over the capture streams of channel.RxCapture (channel.py:35-38).
+ */
+typedef struct {
+  int32_t n_frames;       /* F >= 0                                    */
+  int32_t n_antennas;     /* N >= 1                                    */
+  int32_t fft_len;        /* M: power of two in [2, 4096]              */
+  int32_t cp_len;         /* C: 0 <= C < M   (waveform.py:35-38)       */
+  int32_t n_data;         /* D >= 0 data symbols after the pilot       */
+  int32_t qam_order;      /* 4, 16 or 64     (waveform.py:20)          */
+  int64_t symbol0_offset; /* DetectionResult.symbol0_offset (sync.py:21) */
+  int64_t row_stride;     /* samples between antenna rows              */
+  int64_t frame_stride;   /* samples between frames                    */
+  float eps;              /* MRC_WEIGHT_FLOOR (receiver.py:33) = 1e-12 */
+  int32_t reserved;       /* must be 0                                 */
+} ofdmrx_frame_desc;
+
+OFDMRX_API int ofdmrx_abi_version(void);
+OFDMRX_API const char* ofdmrx_last_error(void);
+
+/* Host-only validation of a descriptor (no device access). Mirrors
+ * OfdmConfig.__post_init__ (waveform.py:32-46) and extract_slots' bounds
+ * check (receiver.py:278-283) against rx_len_samples (pass -1 to skip). */
+OFDMRX_API int ofdmrx_check_desc(const ofdmrx_frame_desc* desc, int64_t rx_len_samples);
+
+/*
+ * Fused receive of F frames (one pass over HBM).  Replaces, per frame,
+ * run_ring_pipeline (receiver.py:308-348) -> process_symbol (238-267) with
+ * SequentialEngine (88-108): cp_drop + to_freq (FFT + fftshift), ls_estimate
+ * on the pilot, mrc_combine + qam_demap on each data symbol.
+ *   rx      cf32 capture (see desc)
+ *   pilot   [M]   cf32 pilot values P (unit modulus), subcarrier order
+ *   H       [F,N,M] cf32 ChannelEstimate.gains                (nullable)
+ *   s_hat   [F,D,M] cf32 CombinedSymbol.equalized            (required if D>0)
+ *   weights [F,M]   f32 CombinedSymbol.weight_norm           (nullable)
+ *   bits    [F,D*M*log2(Q)] u8 0/1, PipelineResult.bits order (required if D>0)
+ *   zf      [F,D,N,M] cf32 per-antenna ZF output conj(H)Y/max(|H|^2,eps) (nullable)
+ *   flags   [F] u32, OR-ed OFDMRX_FLAG_* (nullable; caller zeroes it)
+ * MRC sums antennas in ascending order (mrc_seq, numba_backend.py:143-162).
+ */
+OFDMRX_API int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
+                     float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream);
+
+/*
+ * Antenna-sharded variant, step 1: the same fused pass over this shard's
+ * antennas, emitting the un-normalised MRC partial sums instead of s_hat/bits.
+ *   num [F,D,M] cf32 = sum_n conj(H_n) Y_n,  den [F,M] f32 = sum_n |H_n|^2
+ * (the two accumulators of mrc_seq, numba_backend.py:146-151).
+ */
+OFDMRX_API int ofdmrx_rx_partials(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* num,
+                       float* den, uint32_t* flags, void* stream);
+
+/*
+ * Antenna-sharded variant, step 2 (after the partials of all shards were
+ * gathered into [n_parts, ...]): pairwise-tree sum over parts in the
+ * reference ReductionPlan order (numerics.py:85-106), floor, divide and demap.
+ */
+OFDMRX_API int ofdmrx_mrc_finish(int32_t n_frames, int32_t n_data, int32_t fft_len, int32_t qam_order, int32_t n_parts,
+                      const void* num, const float* den, float eps, void* s_hat, float* weights, uint8_t* bits,
+                      uint32_t* flags, void* stream);
+
+/*
+ * Staged stage 1: CP drop + FFT + fftshift of symbols [first_symbol,
+ * first_symbol + n_symbols) of every frame/antenna in desc.
+ * Replaces engine.freq_transform (receiver.py:92-93,133-142) and
+ * kernels.fft_rows (kernels/__init__.py:40-42) + numerics.fftshift.
+ *   Y [F, n_symbols, N, M] cf32
+ */
+OFDMRX_API int ofdmrx_fft_shift(const ofdmrx_frame_desc* desc, int32_t first_symbol, int32_t n_symbols, const void* rx,
+                     void* Y, void* stream);
+
+/* Staged stage 2: H[f,n,k] = Y[f*y_frame_stride + n*M + k] * conj(P[k]).
+ * Replaces engine.ls_divide (receiver.py:95-96,144-151). */
+OFDMRX_API int ofdmrx_ls(int32_t n_frames, int32_t n_antennas, int32_t fft_len, const void* Y, int64_t y_frame_stride,
+              const void* pilot, void* H, void* stream);
+
+/* Staged stage 3: MRC of D data symbols per frame.  Y element (f,d,n,k) at
+ * Y + f*y_frame_stride + d*y_symbol_stride + n*M + k; H [F,N,M].
+ * tree = 0: mrc_seq order; tree = 1: mrc_tree order (numba_backend.py:109-140).
+ * Replaces engine.mrc (receiver.py:98-99,153-164).
+ *   s_hat [F,D,M] cf32, weights [F,D,M] f32 (nullable), zf [F,D,N,M] (nullable) */
+OFDMRX_API int ofdmrx_mrc(int32_t n_frames, int32_t n_data, int32_t n_antennas, int32_t fft_len, const void* Y,
+               int64_t y_frame_stride, int64_t y_symbol_stride, const void* H, float eps, int32_t tree, void* s_hat,
+               float* weights, void* zf, void* stream);
+
+/* Staged stage 4: hard QAM demap of n symbols -> n*log2(Q) bits.
+ * Replaces waveform.qam_demap (waveform.py:179-197). */
+OFDMRX_API int ofdmrx_demap(const void* symbols, int64_t n, int32_t qam_order, uint8_t* bits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OFDMRX_B200_H_ */

@@ -1,0 +1,284 @@
+// extern "C" boundary of libofdmrx_b200.so (declared in include/ofdmrx_b200.h).
+// Validation mirrors the reference's Python-side checks so the host mirror can
+// map status codes 1:1 onto the errors.py taxonomy.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/ofdmrx_b200.h"
+#include "ofdmrx_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(OFDMRX_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+bool is_pow2(long long x) { return x >= 1 && (x & (x - 1)) == 0; }
+
+int qam_bits(int order) { return order == 4 ? 2 : order == 16 ? 4 : order == 64 ? 6 : 0; }
+
+// waveform._build_constellation (waveform.py:138-151): scale = 1/sqrt(2*mean((L-1-2i)^2))
+void qam_consts(int order, int* qb, int* levels, float* scale) {
+  *qb = qam_bits(order);
+  *levels = 1 << (*qb / 2);
+  double acc = 0.0;
+  for (int i = 0; i < *levels; ++i) {
+    const double a = (*levels - 1) - 2.0 * i;
+    acc += a * a;
+  }
+  *scale = (float)(1.0 / std::sqrt(2.0 * (acc / *levels)));
+}
+
+int check_fft_len(long long m) {
+  if (m < 2 || !is_pow2(m))
+    return fail(OFDMRX_ERR_CONFIG, "fft length must be a power of two >= 2, got %lld", m);
+  if (m > 4096) return fail(OFDMRX_ERR_CONFIG, "fft length %lld exceeds the device path limit 4096", m);
+  return OFDMRX_OK;
+}
+
+int check_qam(int order) {
+  if (qam_bits(order) == 0) return fail(OFDMRX_ERR_CONFIG, "qam order must be one of (4, 16, 64), got %d", order);
+  return OFDMRX_OK;
+}
+
+int check_desc_impl(const ofdmrx_frame_desc* d, long long rx_len) {
+  if (d == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
+  if (d->reserved != 0) return fail(OFDMRX_ERR_CONTRACT, "descriptor reserved field must be 0");
+  if (int rc = check_fft_len(d->fft_len)) return rc;
+  if (d->cp_len < 0 || d->cp_len >= d->fft_len)
+    return fail(OFDMRX_ERR_CONFIG, "cp_len must satisfy 0 <= cp_len < fft_len, got %d", d->cp_len);
+  if (d->n_antennas < 1) return fail(OFDMRX_ERR_CONFIG, "n_antennas must be >= 1, got %d", d->n_antennas);
+  if (int rc = check_qam(d->qam_order)) return rc;
+  if (d->n_frames < 0) return fail(OFDMRX_ERR_CONTRACT, "n_frames must be >= 0, got %d", d->n_frames);
+  if (d->n_data < 0) return fail(OFDMRX_ERR_CONTRACT, "n_data must be >= 0, got %d", d->n_data);
+  if (!(d->eps >= 0.0f) || !std::isfinite(d->eps)) return fail(OFDMRX_ERR_CONFIG, "eps must be finite and >= 0");
+  if (d->symbol0_offset < 0 || d->row_stride < 0 || d->frame_stride < 0)
+    return fail(OFDMRX_ERR_CONTRACT, "offsets and strides must be >= 0");
+  const long long span = d->symbol0_offset + (long long)(1 + d->n_data) * (d->fft_len + d->cp_len);
+  if (d->n_antennas > 1 && d->row_stride < span && d->row_stride != 0)
+    return fail(OFDMRX_ERR_CONTRACT, "row_stride %lld shorter than the %lld samples a row needs",
+                (long long)d->row_stride, span);
+  if (rx_len >= 0 && d->n_frames > 0) {
+    const long long last = (long long)(d->n_frames - 1) * d->frame_stride +
+                           (long long)(d->n_antennas - 1) * d->row_stride + span;
+    if (last > rx_len)
+      return fail(OFDMRX_ERR_INPUT, "capture has %lld samples, %lld needed for %d symbols at offset %lld", rx_len,
+                  last, 1 + d->n_data, (long long)d->symbol0_offset);
+  }
+  return OFDMRX_OK;
+}
+
+int check_ptr(const void* p, const char* what) {
+  if (p == nullptr) return fail(OFDMRX_ERR_CONTRACT, "%s is NULL", what);
+  return OFDMRX_OK;
+}
+
+int check_align(const void* p, unsigned a, const char* what) {
+  if ((reinterpret_cast<uintptr_t>(p) & (a - 1)) != 0)
+    return fail(OFDMRX_ERR_CONTRACT, "%s must be %u-byte aligned", what, a);
+  return OFDMRX_OK;
+}
+
+int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, int mode, void* H, void* s_hat,
+                 float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream) {
+  if (int rc = check_desc_impl(d, -1)) return rc;
+  if (d->n_frames == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(rx, "rx")) return rc;
+  if (int rc = check_align(rx, 8, "rx")) return rc;
+  if (int rc = check_ptr(pilot, "pilot")) return rc;
+  if (mode == 0 && d->n_data > 0) {
+    if (int rc = check_ptr(s_hat, "s_hat")) return rc;
+    if (int rc = check_ptr(bits, "bits")) return rc;
+    if (int rc = check_align(bits, 4, "bits")) return rc;
+  }
+  if (mode == 1) {
+    if (d->n_data > 0)
+      if (int rc = check_ptr(num, "num")) return rc;
+    if (int rc = check_ptr(den, "den")) return rc;
+  }
+  ofdmrx::FusedLaunch l{};
+  cudaError_t e = ofdmrx::fused_plan(d->fft_len, d->n_frames, d->n_data, &l);
+  if (e != cudaSuccess) return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);
+  ofdmrx::FusedParams p{};
+  p.rx = static_cast<const float2*>(rx);
+  p.frame_stride = d->frame_stride;
+  p.row_stride = d->row_stride;
+  p.sym0 = d->symbol0_offset;
+  p.n_frames = d->n_frames;
+  p.n_ant = d->n_antennas;
+  p.cp = d->cp_len;
+  p.n_data = d->n_data;
+  p.dc = l.dc;
+  p.n_chunks = l.n_chunks;
+  p.fpb = l.fpb;
+  p.n_work = d->n_frames * l.n_chunks;
+  p.lanes = l.lanes;
+  p.pilot = static_cast<const float2*>(pilot);
+  p.eps = d->eps;
+  qam_consts(d->qam_order, &p.qb, &p.levels, &p.qscale);
+  p.mode = mode;
+  p.H = static_cast<float2*>(H);
+  p.s_hat = static_cast<float2*>(s_hat);
+  p.weights = weights;
+  p.bits = bits;
+  p.zf = static_cast<float2*>(zf);
+  p.flags = flags;
+  p.part_num = static_cast<float2*>(num);
+  p.part_den = den;
+  e = ofdmrx::launch_fused(d->fft_len, p, l, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "rx_fused_kernel launch");
+  return OFDMRX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ofdmrx_abi_version(void) { return OFDMRX_ABI_VERSION; }
+
+const char* ofdmrx_last_error(void) { return g_last_error.c_str(); }
+
+int ofdmrx_check_desc(const ofdmrx_frame_desc* desc, int64_t rx_len_samples) {
+  return check_desc_impl(desc, rx_len_samples);
+}
+
+int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
+                     float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream) {
+  return fused_common(desc, rx, pilot, 0, H, s_hat, weights, bits, zf, flags, nullptr, nullptr, stream);
+}
+
+int ofdmrx_rx_partials(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* num,
+                       float* den, uint32_t* flags, void* stream) {
+  return fused_common(desc, rx, pilot, 1, H, nullptr, nullptr, nullptr, nullptr, flags, num, den, stream);
+}
+
+int ofdmrx_mrc_finish(int32_t n_frames, int32_t n_data, int32_t fft_len, int32_t qam_order, int32_t n_parts,
+                      const void* num, const float* den, float eps, void* s_hat, float* weights, uint8_t* bits,
+                      uint32_t* flags, void* stream) {
+  if (int rc = check_fft_len(fft_len)) return rc;
+  if (int rc = check_qam(qam_order)) return rc;
+  if (n_frames < 0 || n_data < 0) return fail(OFDMRX_ERR_CONTRACT, "n_frames and n_data must be >= 0");
+  if (n_parts < 1 || n_parts > 0x7fffffff) return fail(OFDMRX_ERR_CONTRACT, "n_parts must be >= 1");
+  if ((long long)n_frames * n_data == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(num, "num")) return rc;
+  if (int rc = check_ptr(den, "den")) return rc;
+  if (int rc = check_ptr(s_hat, "s_hat")) return rc;
+  if (int rc = check_ptr(bits, "bits")) return rc;
+  ofdmrx::FinishParams p{};
+  p.num = static_cast<const float2*>(num);
+  p.den = den;
+  p.parts = n_parts;
+  p.n_frames = n_frames;
+  p.n_data = n_data;
+  p.M = fft_len;
+  p.eps = eps;
+  qam_consts(qam_order, &p.qb, &p.levels, &p.qscale);
+  p.s_hat = static_cast<float2*>(s_hat);
+  p.weights = weights;
+  p.bits = bits;
+  p.flags = flags;
+  cudaError_t e = ofdmrx::launch_finish(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "finish_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_fft_shift(const ofdmrx_frame_desc* desc, int32_t first_symbol, int32_t n_symbols, const void* rx, void* Y,
+                     void* stream) {
+  if (int rc = check_desc_impl(desc, -1)) return rc;
+  if (first_symbol < 0 || n_symbols < 0 || first_symbol + n_symbols > 1 + desc->n_data)
+    return fail(OFDMRX_ERR_CONTRACT, "symbol range [%d, %d) outside the frame's %d symbols", first_symbol,
+                first_symbol + n_symbols, 1 + desc->n_data);
+  if ((long long)desc->n_frames * n_symbols == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(rx, "rx")) return rc;
+  if (int rc = check_ptr(Y, "Y")) return rc;
+  ofdmrx::FftRowsParams p{};
+  const long long sym_len = desc->fft_len + desc->cp_len;
+  p.src = static_cast<const float2*>(rx);
+  p.frame_stride = desc->frame_stride;
+  p.row_stride = desc->row_stride;
+  p.sym0 = desc->symbol0_offset + (long long)first_symbol * sym_len + desc->cp_len;
+  p.sym_stride = sym_len;
+  p.n_frames = desc->n_frames;
+  p.n_sym = n_symbols;
+  p.n_ant = desc->n_antennas;
+  p.out = static_cast<float2*>(Y);
+  cudaError_t e = ofdmrx::launch_fft_rows(desc->fft_len, p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fft_rows_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_ls(int32_t n_frames, int32_t n_antennas, int32_t fft_len, const void* Y, int64_t y_frame_stride,
+              const void* pilot, void* H, void* stream) {
+  if (fft_len < 1) return fail(OFDMRX_ERR_CONFIG, "fft_len must be >= 1");
+  if (n_frames < 0 || n_antennas < 0) return fail(OFDMRX_ERR_CONTRACT, "negative sizes");
+  if ((long long)n_frames * n_antennas == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(Y, "Y")) return rc;
+  if (int rc = check_ptr(pilot, "pilot")) return rc;
+  if (int rc = check_ptr(H, "H")) return rc;
+  cudaError_t e = ofdmrx::launch_ls(static_cast<const float2*>(Y), y_frame_stride, n_frames, n_antennas, fft_len,
+                                    static_cast<const float2*>(pilot), static_cast<float2*>(H),
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "ls_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_mrc(int32_t n_frames, int32_t n_data, int32_t n_antennas, int32_t fft_len, const void* Y,
+               int64_t y_frame_stride, int64_t y_symbol_stride, const void* H, float eps, int32_t tree, void* s_hat,
+               float* weights, void* zf, void* stream) {
+  if (fft_len < 1) return fail(OFDMRX_ERR_CONFIG, "fft_len must be >= 1");
+  if (n_frames < 0 || n_data < 0 || n_antennas < 1) return fail(OFDMRX_ERR_CONTRACT, "bad sizes");
+  if (tree != 0 && tree != 1) return fail(OFDMRX_ERR_CONFIG, "tree must be 0 or 1");
+  if ((long long)n_frames * n_data == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(Y, "Y")) return rc;
+  if (int rc = check_ptr(H, "H")) return rc;
+  if (int rc = check_ptr(s_hat, "s_hat")) return rc;
+  ofdmrx::MrcParams p{};
+  p.Y = static_cast<const float2*>(Y);
+  p.y_fs = y_frame_stride;
+  p.y_ss = y_symbol_stride;
+  p.H = static_cast<const float2*>(H);
+  p.n_frames = n_frames;
+  p.n_data = n_data;
+  p.n_ant = n_antennas;
+  p.M = fft_len;
+  p.eps = eps;
+  p.tree = tree;
+  p.s_hat = static_cast<float2*>(s_hat);
+  p.weights = weights;
+  p.zf = static_cast<float2*>(zf);
+  cudaError_t e = ofdmrx::launch_mrc(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "mrc_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_demap(const void* symbols, int64_t n, int32_t qam_order, uint8_t* bits, void* stream) {
+  if (int rc = check_qam(qam_order)) return rc;
+  if (n < 0) return fail(OFDMRX_ERR_CONTRACT, "n must be >= 0");
+  if (n == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(symbols, "symbols")) return rc;
+  if (int rc = check_ptr(bits, "bits")) return rc;
+  if (int rc = check_align(bits, 4, "bits")) return rc;
+  int qb, levels;
+  float scale;
+  qam_consts(qam_order, &qb, &levels, &scale);
+  cudaError_t e = ofdmrx::launch_demap(static_cast<const float2*>(symbols), n, qb, levels, scale, bits,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "demap_kernel launch");
+  return OFDMRX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Internal launch interfaces shared by the kernel TUs and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ofdmrx {
+
+// Fused receive: one CTA processes FPB work items; a work item is one
+// (frame, chunk of data symbols) pair and owns 1 + DC "symbol lanes"
+// (lane 0 = pilot).  Every lane streams its symbol's antenna rows through
+// a double-buffered TMA stage, FFTs them, and the pilot lane hands the LS
+// estimate H_n to the data lanes through shared memory.
+struct FusedParams {
+  const float2* rx;        // capture base (cf32)
+  long long frame_stride;  // samples between frames
+  long long row_stride;    // samples between antenna rows
+  long long sym0;          // offset (samples) of the pilot symbol's CP inside a row
+  int n_frames, n_ant, cp, n_data;
+  int dc, n_chunks, fpb, n_work, lanes;
+  const float2* pilot;     // [M] pilot values, subcarrier (shifted) order
+  float eps;
+  int qb, levels;
+  float qscale;
+  int mode;                // 0 = full (divide + demap), 1 = partial sums
+  // outputs (nullable unless noted)
+  float2* H;               // [F, N, M]
+  float2* s_hat;           // [F, D, M]            (mode 0, required)
+  float* weights;          // [F, M]
+  uint8_t* bits;           // [F, D*M*qb]          (mode 0, required)
+  float2* zf;              // [F, D, N, M]
+  uint32_t* flags;         // [F]
+  float2* part_num;        // [F, D, M]            (mode 1, required)
+  float* part_den;         // [F, M]               (mode 1, required)
+};
+
+struct FusedLaunch {
+  int dc, n_chunks, fpb, lanes, threads, grid;
+  size_t smem;
+};
+
+// returns cudaErrorInvalidValue for unsupported M
+cudaError_t fused_plan(int M, int n_frames, int n_data, FusedLaunch* out);
+cudaError_t launch_fused(int M, const FusedParams& p, const FusedLaunch& l, cudaStream_t s);
+
+// Staged kernels (per-stage timing and the engine protocol).
+struct FftRowsParams {
+  const float2* src;
+  long long frame_stride, row_stride, sym0, sym_stride;  // row address = src + f*fs + n*rs + sym0 + s*ss
+  int n_frames, n_sym, n_ant;                            // rows = F*S*N, output [F, S, N, M]
+  float2* out;
+};
+cudaError_t launch_fft_rows(int M, const FftRowsParams& p, cudaStream_t s);
+
+cudaError_t launch_ls(const float2* Y, long long y_frame_stride, int n_frames, int n_ant, int M,
+                      const float2* pilot, float2* H, cudaStream_t s);
+
+struct MrcParams {
+  const float2* Y;         // data symbols: Y + f*y_fs + d*y_ss + n*M + k
+  long long y_fs, y_ss;
+  const float2* H;         // H + f*N*M + n*M + k
+  int n_frames, n_data, n_ant, M;
+  float eps;
+  int tree;                // 0 = ascending antenna order, 1 = pairwise tree
+  float2* s_hat;           // [F, D, M]
+  float* weights;          // [F, D, M]
+  float2* zf;              // [F, D, N, M] or null
+};
+cudaError_t launch_mrc(const MrcParams& p, cudaStream_t s);
+
+cudaError_t launch_demap(const float2* sym, long long n, int qb, int levels, float scale, uint8_t* bits,
+                         cudaStream_t s);
+
+struct FinishParams {
+  const float2* num;       // [parts, F, D, M]
+  const float* den;        // [parts, F, M]
+  int parts, n_frames, n_data, M;
+  float eps;
+  int qb, levels;
+  float qscale;
+  float2* s_hat;           // [F, D, M]
+  float* weights;          // [F, M] or null
+  uint8_t* bits;           // [F, D*M*qb]
+  uint32_t* flags;         // [F] or null
+};
+cudaError_t launch_finish(const FinishParams& p, cudaStream_t s);
+
+}  // namespace ofdmrx

@@ -1,0 +1,189 @@
+"""Batched, device-resident receive: the throughput entry point.
+
+``receive_frames`` runs the fused sm_100a kernel over F captures at once:
+CP drop + FFT + fftshift, LS estimate on the pilot symbol, MRC over the
+antennas, divide, hard demap — one pass over HBM.  It is the batched form of
+the reference's per-frame chain extract_slots -> run_ring_pipeline ->
+process_symbol (receiver.py:238-348); the per-symbol API in receiver.py is
+compatibility sugar over it.
+
+Input layout: ``rx`` is a complex64 tensor [F, N, S] (or [N, S] for one frame)
+holding each antenna's sample stream; the pilot symbol (with its CP) starts
+at ``symbol0_offset`` (DetectionResult.symbol0_offset, sync.py:21) and is
+followed by ``n_data`` data symbols of fft_len + cp_len samples.  This is the
+interleaved cf32 layout of the reference's .cf32 files (io_formats.py:18-30).
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, device
+from .errors import ContractError, InputError
+from .waveform import OfdmConfig, PilotDefinition, make_pilot
+
+
+@dataclass
+class FrameBatch:
+    """Outputs of one receive_frames call (CUDA tensors unless copied)."""
+
+    H: torch.Tensor        # [F, N, M] complex64  ChannelEstimate.gains
+    s_hat: torch.Tensor    # [F, D, M] complex64  CombinedSymbol.equalized
+    weights: torch.Tensor  # [F, M]    float32    CombinedSymbol.weight_norm
+    bits: torch.Tensor     # [F, D*M*b] uint8     PipelineResult.bits
+    flags: torch.Tensor    # [F]       int32      OR of FLAG_NONFINITE / FLAG_ERASED
+    zf: torch.Tensor = None  # [F, D, N, M] per-antenna ZF output (optional)
+
+    @property
+    def erased(self):
+        """CombinedSymbol.erased per frame/subcarrier (receiver.py:234)."""
+        return self.weights < device.MRC_WEIGHT_FLOOR
+
+
+def _pilot_values(pilot, fft_len):
+    if pilot is None:
+        pilot = make_pilot(fft_len)
+    if isinstance(pilot, PilotDefinition):
+        vals = pilot.values
+    else:
+        vals = pilot
+    vals = np.asarray(vals.cpu() if isinstance(vals, torch.Tensor) else vals)
+    if vals.shape != (fft_len,):
+        raise ContractError(f"pilot has {vals.shape} values, config needs ({fft_len},)")
+    if not np.allclose(np.abs(vals), 1.0, atol=1e-12):
+        from .errors import ConfigurationError
+
+        raise ConfigurationError("pilot values must have unit modulus")
+    return vals
+
+
+class PilotCache:
+    """Device copies of pilot tables, keyed by (device, values)."""
+
+    def __init__(self):
+        self._cache = {}
+
+    def get(self, vals, dev):
+        key = (str(dev), vals.shape[0], hash(np.asarray(vals, dtype=np.complex64).tobytes()))
+        t = self._cache.get(key)
+        if t is None:
+            t = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.complex64)).to(dev)
+            self._cache[key] = t
+        return t
+
+
+_PILOTS = PilotCache()
+
+
+def allocate_outputs(n_frames, n_antennas, fft_len, n_data, qam_order, dev, want_h=True, zf=False):
+    qb = device.qam_bits(qam_order)
+    return FrameBatch(
+        H=torch.empty((n_frames, n_antennas, fft_len), dtype=torch.complex64, device=dev) if want_h else None,
+        s_hat=torch.empty((n_frames, n_data, fft_len), dtype=torch.complex64, device=dev),
+        weights=torch.empty((n_frames, fft_len), dtype=torch.float32, device=dev),
+        bits=torch.empty((n_frames, n_data * fft_len * qb), dtype=torch.uint8, device=dev),
+        flags=torch.zeros((n_frames,), dtype=torch.int32, device=dev),
+        zf=torch.empty((n_frames, n_data, n_antennas, fft_len), dtype=torch.complex64, device=dev) if zf else None,
+    )
+
+
+def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
+                   out=None, want_h=True, zf=False, check=False, stream=None):
+    """Fused receive of a batch of captures on the current CUDA device.
+
+    rx: complex64 CUDA tensor [F, N, S] or [N, S] (numpy is copied H2D).
+    Returns a FrameBatch.  With check=True, raises NumericInputError when a
+    frame fed non-finite samples to the FFT (forces a device sync)."""
+    if not isinstance(cfg, OfdmConfig):
+        raise ContractError("cfg must be an OfdmConfig")
+    dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
+    x = device.as_c64(rx, dev)
+    if x.dim() == 2:
+        x = x[None]
+    if x.dim() != 3:
+        raise ContractError(f"rx must be [F, N, S] or [N, S], got shape {tuple(x.shape)}")
+    f, n, s = x.shape
+    if n != cfg.n_antennas:
+        raise ContractError(f"rx has {n} antenna rows, config has {cfg.n_antennas}")
+    sym_len = cfg.symbol_len
+    if n_data is None:
+        n_data = (s - symbol0_offset) // sym_len - 1
+    if n_data < 0 or symbol0_offset < 0:
+        raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
+    device.check_desc(desc, f * n * s)
+    pv = _PILOTS.get(_pilot_values(pilot, cfg.fft_len), dev)
+    if out is None:
+        out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
+    else:
+        out.flags.zero_()
+    _lib.call("ofdmrx_rx_frames", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(out.H),
+              device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
+              device.ptr(out.flags), device.stream_handle(stream))
+    if check:
+        device.raise_on_flags(out.flags)
+    return out
+
+
+def receive_partials(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
+                     want_h=True, stream=None):
+    """Antenna-shard half of the fused pass: returns (H, num [F,D,M] c64,
+    den [F,M] f32, flags) — the un-normalised MRC accumulators over this
+    shard's antennas (mrc_seq, numba_backend.py:146-151)."""
+    dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
+    x = device.as_c64(rx, dev)
+    if x.dim() == 2:
+        x = x[None]
+    f, n, s = x.shape
+    if n_data is None:
+        n_data = (s - symbol0_offset) // cfg.symbol_len - 1
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
+    device.check_desc(desc, f * n * s)
+    pv = _PILOTS.get(_pilot_values(pilot, cfg.fft_len), dev)
+    H = torch.empty((f, n, cfg.fft_len), dtype=torch.complex64, device=dev) if want_h else None
+    num = torch.empty((f, n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
+    den = torch.empty((f, cfg.fft_len), dtype=torch.float32, device=dev)
+    flags = torch.zeros((f,), dtype=torch.int32, device=dev)
+    _lib.call("ofdmrx_rx_partials", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(H),
+              device.ptr(num), device.ptr(den), device.ptr(flags), device.stream_handle(stream))
+    return H, num, den, flags
+
+
+def finish_partials(num_parts, den_parts, qam_order, eps=device.MRC_WEIGHT_FLOOR, stream=None):
+    """Sum gathered partials [G, F, D, M] / [G, F, M] over G in the reference
+    pairwise-tree order, floor, divide and demap.  Returns (s_hat, weights,
+    bits, flags)."""
+    g, f, d, m = num_parts.shape
+    if tuple(den_parts.shape) != (g, f, m):
+        raise ContractError(f"den partials {tuple(den_parts.shape)} do not match num {tuple(num_parts.shape)}")
+    dev = num_parts.device
+    qb = device.qam_bits(qam_order)
+    s_hat = torch.empty((f, d, m), dtype=torch.complex64, device=dev)
+    weights = torch.empty((f, m), dtype=torch.float32, device=dev)
+    bits = torch.empty((f, d * m * qb), dtype=torch.uint8, device=dev)
+    flags = torch.zeros((f,), dtype=torch.int32, device=dev)
+    _lib.call("ofdmrx_mrc_finish", f, d, m, int(qam_order), g, device.ptr(num_parts.contiguous()),
+              device.ptr(den_parts.contiguous()), float(eps), device.ptr(s_hat), device.ptr(weights),
+              device.ptr(bits), device.ptr(flags), device.stream_handle(stream))
+    return s_hat, weights, bits, flags
+
+
+def fft_symbols(rx, cfg, *, symbol0_offset=0, n_data=None, first_symbol=0, n_symbols=None, stream=None):
+    """Staged stage 1 over a batch: Y [F, S, N, M] (CP dropped, FFT, fftshift)."""
+    dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
+    x = device.as_c64(rx, dev)
+    if x.dim() == 2:
+        x = x[None]
+    f, n, s = x.shape
+    if n_data is None:
+        n_data = (s - symbol0_offset) // cfg.symbol_len - 1
+    if n_symbols is None:
+        n_symbols = 1 + n_data - first_symbol
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s)
+    device.check_desc(desc, f * n * s)
+    y = torch.empty((f, n_symbols, n, cfg.fft_len), dtype=torch.complex64, device=dev)
+    _lib.call("ofdmrx_fft_shift", ctypes.byref(desc), int(first_symbol), int(n_symbols), device.ptr(x),
+              device.ptr(y), device.stream_handle(stream))
+    return y
