@@ -74,8 +74,12 @@ typedef struct {
   int64_t row_stride;     /* samples between antenna rows              */
   int64_t frame_stride;   /* samples between frames                    */
   float eps;              /* MRC_WEIGHT_FLOOR (receiver.py:33) = 1e-12 */
-  int32_t reserved;       /* must be 0                                 */
+  int32_t options;        /* OR of OFDMRX_OPT_* (0 = none)             */
 } ofdmrx_frame_desc;
+
+/* desc.options: the caller asserts every pilot value is exactly +1 or -1
+ * (make_pilot's BPSK pilot, waveform.py:214-220); H = Y/P becomes a sign flip. */
+#define OFDMRX_OPT_PILOT_BPSK 1
 
 OFDMRX_API int ofdmrx_abi_version(void);
 OFDMRX_API const char* ofdmrx_last_error(void);

@@ -21,6 +21,7 @@ ABI_VERSION = 1
 OK, ERR_CONFIG, ERR_CONTRACT, ERR_INPUT, ERR_NUMERIC, ERR_CUDA = range(6)
 FLAG_NONFINITE = 1
 FLAG_ERASED = 2
+OPT_PILOT_BPSK = 1
 
 _STATUS_EXC = {
     ERR_CONFIG: ConfigurationError,
@@ -45,7 +46,7 @@ class FrameDesc(ctypes.Structure):
         ("row_stride", ctypes.c_int64),
         ("frame_stride", ctypes.c_int64),
         ("eps", ctypes.c_float),
-        ("reserved", ctypes.c_int32),
+        ("options", ctypes.c_int32),
     ]
 
 

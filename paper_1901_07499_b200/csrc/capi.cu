@@ -57,7 +57,7 @@ int check_qam(int order) {
 
 int check_desc_impl(const ofdmrx_frame_desc* d, long long rx_len) {
   if (d == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
-  if (d->reserved != 0) return fail(OFDMRX_ERR_CONTRACT, "descriptor reserved field must be 0");
+  if ((d->options & ~OFDMRX_OPT_PILOT_BPSK) != 0) return fail(OFDMRX_ERR_CONTRACT, "unknown descriptor options 0x%x", d->options);
   if (int rc = check_fft_len(d->fft_len)) return rc;
   if (d->cp_len < 0 || d->cp_len >= d->fft_len)
     return fail(OFDMRX_ERR_CONFIG, "cp_len must satisfy 0 <= cp_len < fft_len, got %d", d->cp_len);
@@ -127,10 +127,13 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   p.fpb = l.fpb;
   p.n_work = d->n_frames * l.n_chunks;
   p.lanes = l.lanes;
+  p.ngroups = l.ngroups;
+  p.npilot = l.npilot;
   p.pilot = static_cast<const float2*>(pilot);
   p.eps = d->eps;
   qam_consts(d->qam_order, &p.qb, &p.levels, &p.qscale);
   p.mode = mode;
+  p.pilot_bpsk = (d->options & OFDMRX_OPT_PILOT_BPSK) != 0;
   p.H = static_cast<float2*>(H);
   p.s_hat = static_cast<float2*>(s_hat);
   p.weights = weights;

@@ -17,12 +17,13 @@ struct FusedParams {
   long long row_stride;    // samples between antenna rows
   long long sym0;          // offset (samples) of the pilot symbol's CP inside a row
   int n_frames, n_ant, cp, n_data;
-  int dc, n_chunks, fpb, n_work, lanes;
+  int dc, n_chunks, fpb, n_work, lanes, ngroups, npilot;
   const float2* pilot;     // [M] pilot values, subcarrier (shifted) order
   float eps;
   int qb, levels;
   float qscale;
   int mode;                // 0 = full (divide + demap), 1 = partial sums
+  int pilot_bpsk;          // pilot values are exactly +-1 (sign-flip LS)
   // outputs (nullable unless noted)
   float2* H;               // [F, N, M]
   float2* s_hat;           // [F, D, M]            (mode 0, required)
@@ -35,7 +36,7 @@ struct FusedParams {
 };
 
 struct FusedLaunch {
-  int dc, n_chunks, fpb, lanes, threads, grid;
+  int dc, n_chunks, fpb, lanes, threads, grid, ngroups, npilot;
   size_t smem;
 };
 

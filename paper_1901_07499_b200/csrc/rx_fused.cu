@@ -7,52 +7,98 @@
 // 95-96), mrc_combine/mrc_seq (221-235; kernels/numba_backend.py:143-162) with
 // MRC_WEIGHT_FLOOR (33), and waveform.qam_demap (waveform.py:179-197).
 //
-// Work decomposition (see DESIGN.md "Fused kernel"):
-//   CTA          = FPB work items, work item = (frame, chunk of DC data symbols)
-//   symbol lane  = G threads holding one OFDM symbol's M-point FFT (P points each)
-//   lane 0/item  = pilot lane (LS estimate, sum |H|^2), lanes 1..DC = data lanes
-//   time loop    = antennas n = 0..N-1; each lane's row (frame, n, symbol) is
-//                  TMA bulk-copied into a double-buffered smem slot one antenna
-//                  ahead; the pilot lane publishes H_n in its slot; data lanes
-//                  accumulate sum_n conj(H_n) Y_n in registers (ascending n =
-//                  the SequentialEngine order).
-// HBM traffic per frame = the rx samples of 1+D symbols x N antennas (CP never
-// read) + H + s_hat + bits (+ weights): the algorithmic minimum.
+// Work decomposition (DESIGN.md "Fused kernel"):
+//   work item   = (frame, chunk of DC data symbols)
+//   symbol lane = G threads computing one OFDM symbol's M-point FFT
+//                 (P points per thread, Stockham passes through a smem slot)
+//   role unit   = max(32, G) threads = GI lanes of the same symbol slot for the
+//                 GI items of a group; unit 0 of a group is the pilot unit.
+//   CTA         = NGROUPS groups x (1 + DC) units.
+// Every lane loops over the antennas n = 0..N-1 on its own: its row (frame,
+// n, symbol) is TMA bulk-copied into a private double-buffered slot one antenna
+// ahead.  The pilot unit publishes H_n = Y_n conj(P) into a RING-deep smem ring
+// (mbarrier full/empty protocol, no CTA-wide barrier in the loop); data units
+// accumulate sum_n conj(H_n) Y_n in registers (ascending n = SequentialEngine
+// order).  HBM traffic per frame = rx samples of 1+D symbols x N antennas (CP
+// never read) + H + s_hat + bits + weights: the algorithmic minimum.
 #include "ofdmrx_fft.cuh"
 #include "ofdmrx_internal.h"
 
 namespace ofdmrx {
 
 template <int M>
+struct FusedCfg {
+  using PI = PlanInfo<M>;
+  static constexpr int G = PI::G;
+  static constexpr int UT = G < 32 ? 32 : G;  // threads per role unit
+  static constexpr int GI = UT / G;           // lanes (items) per unit
+  static constexpr int SLOT_STRIDE = PI::SLOT + (G == 1 ? 2 : (G == 8 ? 8 : 0));  // bank skew between lanes
+  static constexpr int HSTRIDE = M + 2;       // one item's H block in a ring slot (float2)
+  static constexpr int RING = 2;  // must be a multiple of the pilot-unit count (1 or 2)
+  static constexpr int NSTAGE = M >= 4096 ? 1 : 2;
+  static size_t smem_bytes(int ngroups, int per_group) {
+    const int units = ngroups * per_group, lanes = units * GI;
+    const size_t bars = ((size_t)(NSTAGE * lanes + 2 * ngroups * RING) * 8 + 127) & ~size_t(127);
+    return bars + (size_t)NSTAGE * lanes * SLOT_STRIDE * 8 + (size_t)ngroups * RING * GI * HSTRIDE * 8;
+  }
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int M, bool ZF, bool BPSK>
 __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(const FusedParams p) {
   using PI = PlanInfo<M>;
-  constexpr int P = PI::P, G = PI::G, SLOT = PI::SLOT;
+  using FC = FusedCfg<M>;
+  constexpr int P = PI::P, G = PI::G, UT = FC::UT, GI = FC::GI, RING = FC::RING, NSTAGE = FC::NSTAGE;
+  constexpr int SS = FC::SLOT_STRIDE, HS = FC::HSTRIDE;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lanes = p.lanes;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);
-  float2* slots = reinterpret_cast<float2*>(smem_raw + ((2 * lanes * 8 + 127) & ~127));
 
-  const int lane = threadIdx.x / G;
-  const int t = threadIdx.x & (G - 1);
-  const int per_item = 1 + p.dc;
-  const int item = lane / per_item;
-  const int sl = lane - item * per_item;
-  const bool phantom = lane >= p.fpb * per_item;  // pads the CTA to whole warps
-  const int work = blockIdx.x * p.fpb + item;
-  const bool item_ok = !phantom && work < p.n_work;
+  const int npilot = p.npilot;          // pilot units per group (alternate antennas)
+  const int per_group = npilot + p.dc;  // units per group
+  const int ngroups = p.ngroups;
+  const int lanes = ngroups * per_group * GI;
+  uint64_t* tma_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [NSTAGE][lanes]
+  uint64_t* full_bar = tma_bar + NSTAGE * lanes;               // [ngroups][RING]
+  uint64_t* empty_bar = full_bar + ngroups * RING;             // [ngroups][RING]
+  const size_t bar_bytes = ((size_t)(NSTAGE * lanes + 2 * ngroups * RING) * 8 + 127) & ~size_t(127);
+  float2* slots = reinterpret_cast<float2*>(smem_raw + bar_bytes);  // [NSTAGE][lanes][SS]
+  float2* ring = slots + (size_t)NSTAGE * lanes * SS;               // [ngroups][RING][GI][HS]
+
+  const int unit = threadIdx.x / UT;
+  const int u = threadIdx.x - unit * UT;
+  const int grp = unit / per_group;
+  const int sl = unit - grp * per_group;
+  const int sub = u / G;
+  const int t = u - sub * G;
+  const int lane = unit * GI + sub;
+  const int work = blockIdx.x * p.fpb + grp * GI + sub;
+  const bool item_ok = work < p.n_work;
   const int f = item_ok ? work / p.n_chunks : 0;
   const int chunk = item_ok ? work - f * p.n_chunks : 0;
-  const bool is_pilot = !phantom && sl == 0;
-  const int d = is_pilot ? 0 : chunk * p.dc + (sl - 1);  // data-symbol index (0-based)
+  const bool is_pilot = sl < npilot;
+  const int d = is_pilot ? 0 : chunk * p.dc + (sl - npilot);  // data-symbol index (0-based)
   const bool active = item_ok && (is_pilot || d < p.n_data);
-  const int pilot_lane = item * per_item;
-  const int s = is_pilot ? 0 : d + 1;  // symbol index within the frame
-  const LaneSync<G> lsync{1 + lane};
+  const int s = is_pilot ? 0 : d + 1;                          // symbol index within the frame
+  // antennas visited by this unit: pilots take every npilot-th antenna
+  const int n_first = is_pilot ? sl : 0;
+  const int n_step = is_pilot ? npilot : 1;
+
+  // unit == lane group of whole warps: one warp (G <= 32) or G/32 warps
+  auto unit_sync = [&]() {
+    if constexpr (UT == 32) __syncwarp();
+    else named_bar_sync(1 + unit, UT);
+  };
 
   const float2* row0 = p.rx + (long long)f * p.frame_stride + p.sym0 + (long long)s * (M + p.cp) + p.cp;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2 * lanes; ++i) mbar_init(&mbar[i], 1);
+    for (int i = 0; i < NSTAGE * lanes; ++i) mbar_init(&tma_bar[i], 1);
+    for (int i = 0; i < ngroups * RING; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], p.dc > 0 ? p.dc : 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -64,68 +110,119 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
     const uintptr_t a = reinterpret_cast<uintptr_t>(row0 + (long long)n * p.row_stride);
     const uintptr_t start = a & ~uintptr_t(15);
     const uint32_t bytes = (uint32_t)(((a + (uintptr_t)M * 8u + 15u) & ~uintptr_t(15)) - start);
-    uint64_t* bar = &mbar[st * lanes + lane];
+    uint64_t* bar = &tma_bar[st * lanes + lane];
     mbar_arrive_expect_tx(bar, bytes);
-    tma_bulk_g2s(slots + (size_t)(st * lanes + lane) * SLOT, reinterpret_cast<const void*>(start), bytes, bar,
-                 pol);
+    tma_bulk_g2s(slots + (size_t)(st * lanes + lane) * SS, reinterpret_cast<const void*>(start), bytes, bar, pol);
   };
-  if (leader) issue(0, 0);
+  if (leader && n_first < p.n_ant) issue(n_first, 0);
+
+  // pilot units: BPSK (+-1 real) pilots reduce H = Y conj(P) to a sign flip; the
+  // sign bits of this thread's P subcarriers are loaded once.
+  uint32_t pmask = 0;
+  if (BPSK && is_pilot) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) pmask |= (__ldg(p.pilot + shifted_bin<M>(i, t)).x < 0.0f ? 1u : 0u) << i;
+  }
 
   const bool write_h = is_pilot && active && chunk == 0 && p.H != nullptr;
-  const bool write_zf = !is_pilot && active && p.zf != nullptr;
   float2 v[P];
   float2 acc[P];
 #pragma unroll
   for (int i = 0; i < P; ++i) acc[i] = make_float2(0.0f, 0.0f);
+  float2* hring_grp = ring + (size_t)grp * RING * GI * HS + (size_t)sub * HS;
 
-  for (int n = 0; n < p.n_ant; ++n) {
-    const int st = n & 1;
-    if (leader && n + 1 < p.n_ant) issue(n + 1, st ^ 1);  // slot freed by the previous step's barrier
-    float2* slot = slots + (size_t)(st * lanes + lane) * SLOT;
-    if (active) mbar_wait_parity(&mbar[st * lanes + lane], (n >> 1) & 1);
+  for (int k = 0, n = n_first; n < p.n_ant; ++k, n += n_step) {
+    const int st = NSTAGE == 2 ? (k & 1) : 0;
+    if (NSTAGE == 2 && leader && n + n_step < p.n_ant) issue(n + n_step, st ^ 1);  // freed at the end of step k-1
+    float2* slot = slots + (size_t)(st * lanes + lane) * SS;
+    if (active) mbar_wait_parity(&tma_bar[st * lanes + lane], NSTAGE == 2 ? ((k >> 1) & 1) : (k & 1));
     const int sh = (int)((reinterpret_cast<uintptr_t>(row0 + (long long)n * p.row_stride) >> 3) & 1);
     const float2* src = slot + sh;
-    fft_forward<M>(v, slot, t, [&](int idx) { return src[idx]; }, lsync);
-    lsync();  // last pass has read the slot; the pilot lane overwrites it with H_n
+    fft_forward<M>(v, slot, t, [&](int idx) { return src[idx]; }, unit_sync);
+    fence_proxy_async_smem();  // this thread's generic smem writes before the async-proxy refill
+    unit_sync();               // every read of the slot done: it may be refilled
+    if (NSTAGE == 1 && leader && n + n_step < p.n_ant) issue(n + n_step, 0);
+
+    const int r = n % RING;
+    const int j = n / RING;
+    float2* hb = hring_grp + (size_t)r * GI * HS;
     if (is_pilot) {
+      if constexpr (BPSK) asm volatile("" : "+r"(pmask));  // keep the per-bit sign words out of registers
+      if (p.dc > 0) mbar_wait_parity(&empty_bar[grp * RING + r], (j + 1) & 1);  // data units done with H_{n-RING}
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const int j = shifted_bin<M>(i, t);
-        const float2 pc = __ldg(p.pilot + j);
-        const float2 y = v[i];
-        // H = Y / P for unit-modulus P == Y * conj(P) (bit-exact for BPSK +-1)
-        const float2 h = make_float2(fmaf(y.y, pc.y, y.x * pc.x), fmaf(-y.x, pc.y, y.y * pc.x));
-        slot[i * G + t] = h;
-        acc[i].x += fmaf(h.x, h.x, h.y * h.y);
-        if (write_h) p.H[((long long)f * p.n_ant + n) * M + j] = h;
+      for (int i = 0; i < P; i += 2) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float2 y = v[i + e];
+          float2 h;
+          if constexpr (BPSK) {
+            const uint32_t sgn = (pmask << (31 - (i + e))) & 0x80000000u;
+            h = make_float2(__uint_as_float(__float_as_uint(y.x) ^ sgn), __uint_as_float(__float_as_uint(y.y) ^ sgn));
+          } else {
+            // H = Y / P for unit-modulus P == Y * conj(P)
+            const float2 pc = __ldg(p.pilot + shifted_bin<M>(i + e, t));
+            h = make_float2(fmaf(y.y, pc.y, y.x * pc.x), fmaf(-y.x, pc.y, y.y * pc.x));
+          }
+          acc[i + e].x = fmaf(h.x, h.x, fmaf(h.y, h.y, acc[i + e].x));
+          v[i + e] = h;
+        }
+        *reinterpret_cast<float4*>(hb + (i >> 1) * 2 * G + 2 * t) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
       }
-    }
-    __syncthreads();  // H_n visible to the data lanes
-    if (!is_pilot && active) {
-      const float2* hs = slots + (size_t)(st * lanes + pilot_lane) * SLOT;
+      unit_sync();
+      if (u == 0) mbar_arrive(&full_bar[grp * RING + r]);
+      if (write_h) {  // off the critical path: the data units already have H_n
+        float2* hdst = p.H + ((long long)f * p.n_ant + n) * M + t;
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const float2 h = hs[i * G + t];
-        const float2 y = v[i];
-        // conj(H) * Y, expanded as in numba_backend.py:149-150
-        acc[i].x += fmaf(h.x, y.x, h.y * y.y);
-        acc[i].y += fmaf(h.x, y.y, -h.y * y.x);
-        if (write_zf) {
-          const float dn = fmaxf(fmaf(h.x, h.x, h.y * h.y), p.eps);
-          const float zr = fmaf(h.x, y.x, h.y * y.y), zi = fmaf(h.x, y.y, -h.y * y.x);
-          const int j = shifted_bin<M>(i, t);
-          p.zf[(((long long)f * p.n_data + d) * p.n_ant + n) * M + j] = make_float2(zr / dn, zi / dn);
+        for (int i = 0; i < P; ++i) hdst[shifted_bin<M>(i, 0)] = v[i];
+      }
+    } else {
+      mbar_wait_parity(&full_bar[grp * RING + r], j & 1);
+#pragma unroll
+      for (int i = 0; i < P; i += 2) {
+        const float4 hh = *reinterpret_cast<const float4*>(hb + (i >> 1) * 2 * G + 2 * t);
+        const float2 h[2] = {make_float2(hh.x, hh.y), make_float2(hh.z, hh.w)};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float2 y = v[i + e];
+          // conj(H) * Y, expanded as in numba_backend.py:149-150
+          acc[i + e].x = fmaf(h[e].y, y.y, fmaf(h[e].x, y.x, acc[i + e].x));
+          acc[i + e].y = fmaf(-h[e].y, y.x, fmaf(h[e].x, y.y, acc[i + e].y));
+          if constexpr (ZF) {
+            if (active) {
+              const float dn = fmaxf(fmaf(h[e].x, h[e].x, h[e].y * h[e].y), p.eps);
+              const float zr = fmaf(h[e].x, y.x, h[e].y * y.y), zi = fmaf(h[e].x, y.y, -h[e].y * y.x);
+              p.zf[(((long long)f * p.n_data + d) * p.n_ant + n) * M + shifted_bin<M>(i + e, t)] =
+                  make_float2(zr / dn, zi / dn);
+            }
+          }
         }
       }
+      unit_sync();
+      if (u == 0) mbar_arrive(&empty_bar[grp * RING + r]);
     }
-    fence_proxy_async_smem();  // generic-proxy smem writes ordered before the next TMA into this stage
-    __syncthreads();
   }
 
-  // ---- epilogue: share den, divide, demap ---------------------------------
+  // ---- epilogue: combine the pilots' den partials, divide, demap ----------
+  __syncthreads();  // ring traffic finished
   uint32_t flag = 0;
+  // den partial of pilot unit q lives in ring slot q of this item
   if (is_pilot) {
-    float* dslot = reinterpret_cast<float*>(slots + (size_t)lane * SLOT);
+    float* dpart = reinterpret_cast<float*>(hring_grp + (size_t)sl * GI * HS);
+#pragma unroll
+    for (int i = 0; i < P; ++i) dpart[i * G + t] = acc[i].x;
+  }
+  __syncthreads();
+  float* dslot = reinterpret_cast<float*>(hring_grp);
+  if (sl == 0) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      float den = dslot[i * G + t];
+      for (int q = 1; q < npilot; ++q) den += reinterpret_cast<const float*>(hring_grp + (size_t)q * GI * HS)[i * G + t];
+      acc[i].x = den;
+    }
+  }
+  __syncthreads();
+  if (sl == 0) {
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       dslot[i * G + t] = acc[i].x;
@@ -137,32 +234,34 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
     if (active && chunk == 0) {
       float* wdst = p.mode == 0 ? p.weights : p.part_den;
       if (wdst != nullptr) {
+        float* w = wdst + (long long)f * M + t;
 #pragma unroll
-        for (int i = 0; i < P; ++i) wdst[(long long)f * M + shifted_bin<M>(i, t)] = acc[i].x;
+        for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = acc[i].x;
       }
     }
   }
   __syncthreads();
   if (!is_pilot && active) {
-    const float* dslot = reinterpret_cast<const float*>(slots + (size_t)pilot_lane * SLOT);
     const long long sym_base = ((long long)f * p.n_data + d) * M;
     if (p.mode == 0) {
       const QamParams q{p.qb, p.levels, p.qscale};
+      float2* sdst = p.s_hat + sym_base + t;
+      uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        const float den = dslot[i * G + t];
-        const float dd = fmaxf(den, p.eps);  // np.maximum(den, eps)
+        const float dd = fmaxf(dslot[i * G + t], p.eps);  // np.maximum(den, eps)
         const float2 sh = make_float2(acc[i].x / dd, acc[i].y / dd);
         if (!isfinite(sh.x) || !isfinite(sh.y)) flag |= 1u;
-        const int j = shifted_bin<M>(i, t);
-        p.s_hat[sym_base + j] = sh;
-        demap_store(sh, q, p.bits + (sym_base + j) * p.qb);
+        const int j = shifted_bin<M>(i, 0);
+        sdst[j] = sh;
+        demap_store(sh, q, bdst + (long long)j * p.qb);
       }
     } else {
+      float2* ndst = p.part_num + sym_base + t;
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         if (!isfinite(acc[i].x) || !isfinite(acc[i].y)) flag |= 1u;
-        p.part_num[sym_base + shifted_bin<M>(i, t)] = acc[i];
+        ndst[shifted_bin<M>(i, 0)] = acc[i];
       }
     }
   }
@@ -172,57 +271,68 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
 template <int M>
 static cudaError_t plan_impl(int n_frames, int n_data, FusedLaunch* l) {
   using PI = PlanInfo<M>;
-  constexpr int G = PI::G;
-  const int lanes_max = PI::MAX_THREADS / G;
+  using FC = FusedCfg<M>;
+  constexpr int UT = FC::UT, GI = FC::GI;
+  const size_t smem_cap = 227 * 1024;
+  const int units_max = PI::MAX_THREADS / UT;
+  if (FC::smem_bytes(1, 1 + (n_data > 0 ? 1 : 0)) > smem_cap) return cudaErrorInvalidValue;
+  // two pilot units (alternating antennas) keep the LS estimate off the critical
+  // path when there are enough data units to feed
+  int npilot = 2;
+  int dc_cap = units_max - npilot;
+  if (dc_cap > 15) dc_cap = 15;
+  while (dc_cap > 1 && FC::smem_bytes(1, npilot + dc_cap) > smem_cap) --dc_cap;
+  if (dc_cap < 4) {
+    npilot = 1;
+    dc_cap = units_max - 1;
+    if (dc_cap > 15) dc_cap = 15;
+    while (dc_cap > 1 && FC::smem_bytes(1, 1 + dc_cap) > smem_cap) --dc_cap;
+  }
   int dc = 0, chunks = 1;
   if (n_data > 0) {
-    dc = n_data;
-    if (dc > lanes_max - 1) dc = lanes_max - 1;
-    if (dc > 15) dc = 15;
+    dc = n_data < dc_cap ? n_data : dc_cap;
     chunks = (n_data + dc - 1) / dc;
     dc = (n_data + chunks - 1) / chunks;
   }
-  const int per_item = 1 + dc;
-  const size_t slot_bytes = (size_t)PI::SLOT * sizeof(float2);
-  const size_t smem_cap = 227 * 1024;
-  auto smem_for = [&](int lanes) { return (size_t)((2 * lanes * 8 + 127) & ~127) + 2 * (size_t)lanes * slot_bytes; };
-  if (smem_for(per_item) > smem_cap) return cudaErrorInvalidValue;
-  int fpb = lanes_max / per_item;
-  if (fpb < 1) fpb = 1;
+  if (dc < 4) npilot = 1;
+  const int per_group = npilot + dc;
+  int ngroups = units_max / per_group;
+  if (ngroups < 1) ngroups = 1;
+  while (ngroups > 1 && FC::smem_bytes(ngroups, per_group) > smem_cap) --ngroups;
   const long long n_work = (long long)n_frames * chunks;
-  const long long want = (n_work + 147) / 148;  // spread items over the 148 SMs first
-  if (fpb > want) fpb = (int)(want < 1 ? 1 : want);
-  int lanes = fpb * per_item;
-  while (true) {
-    int padded = lanes;
-    if (G < 32) padded = ((lanes * G + 31) / 32 * 32) / G;
-    if (smem_for(padded) <= smem_cap || fpb == 1) { lanes = padded; break; }
-    --fpb;
-    lanes = fpb * per_item;
-  }
-  if (smem_for(lanes) > smem_cap) return cudaErrorInvalidValue;
+  const long long want = (n_work + 148LL * GI - 1) / (148LL * GI);  // spread groups over the 148 SMs first
+  if (ngroups > want) ngroups = (int)(want < 1 ? 1 : want);
   l->dc = dc;
+  l->npilot = npilot;
   l->n_chunks = chunks;
-  l->fpb = fpb;
-  l->lanes = lanes;
-  l->threads = lanes * G;
-  l->grid = (int)((n_work + fpb - 1) / fpb);
-  l->smem = smem_for(lanes);
+  l->ngroups = ngroups;
+  l->fpb = ngroups * GI;
+  l->lanes = ngroups * per_group * GI;
+  l->threads = ngroups * per_group * UT;
+  l->grid = (int)((n_work + l->fpb - 1) / l->fpb);
+  l->smem = FC::smem_bytes(ngroups, per_group);
   return cudaSuccess;
 }
 
-template <int M>
-static cudaError_t launch_impl(const FusedParams& p, const FusedLaunch& l, cudaStream_t s) {
+template <int M, bool ZF, bool BPSK>
+static cudaError_t launch_one(const FusedParams& p, const FusedLaunch& l, cudaStream_t s) {
   static bool attr_set = false;  // benign race: idempotent attribute write
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rx_fused_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(rx_fused_kernel<M, ZF, BPSK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   if (l.grid == 0) return cudaSuccess;
-  rx_fused_kernel<M><<<l.grid, l.threads, l.smem, s>>>(p);
+  rx_fused_kernel<M, ZF, BPSK><<<l.grid, l.threads, l.smem, s>>>(p);
   return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t launch_impl(const FusedParams& p, const FusedLaunch& l, cudaStream_t s) {
+  if (p.pilot_bpsk)
+    return p.zf != nullptr ? launch_one<M, true, true>(p, l, s) : launch_one<M, false, true>(p, l, s);
+  return p.zf != nullptr ? launch_one<M, true, false>(p, l, s) : launch_one<M, false, false>(p, l, s);
 }
 
 #define OFDMRX_FOR_EACH_M(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)

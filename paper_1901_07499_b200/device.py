@@ -63,10 +63,16 @@ def qam_bits(order):
 
 
 def make_desc(n_frames, n_antennas, fft_len, cp_len, n_data, qam_order, symbol0_offset, row_stride,
-              frame_stride, eps=MRC_WEIGHT_FLOOR):
+              frame_stride, eps=MRC_WEIGHT_FLOOR, options=0):
     return _lib.FrameDesc(int(n_frames), int(n_antennas), int(fft_len), int(cp_len), int(n_data),
                           int(qam_order), int(symbol0_offset), int(row_stride), int(frame_stride),
-                          float(eps), 0)
+                          float(eps), int(options))
+
+
+def pilot_options(pilot_values):
+    """OFDMRX_OPT_PILOT_BPSK when every pilot value is exactly +-1 + 0j."""
+    v = np.asarray(pilot_values)
+    return _lib.OPT_PILOT_BPSK if np.all((v.imag == 0) & (np.abs(v.real) == 1)) else 0
 
 
 def check_desc(desc, rx_len=-1):

@@ -112,9 +112,11 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
         n_data = (s - symbol0_offset) // sym_len - 1
     if n_data < 0 or symbol0_offset < 0:
         raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
-    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
+    pvals = _pilot_values(pilot, cfg.fft_len)
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps,
+                            options=device.pilot_options(pvals))
     device.check_desc(desc, f * n * s)
-    pv = _PILOTS.get(_pilot_values(pilot, cfg.fft_len), dev)
+    pv = _PILOTS.get(pvals, dev)
     if out is None:
         out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
     else:
@@ -139,9 +141,11 @@ def receive_partials(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=
     f, n, s = x.shape
     if n_data is None:
         n_data = (s - symbol0_offset) // cfg.symbol_len - 1
-    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
+    pvals = _pilot_values(pilot, cfg.fft_len)
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps,
+                            options=device.pilot_options(pvals))
     device.check_desc(desc, f * n * s)
-    pv = _PILOTS.get(_pilot_values(pilot, cfg.fft_len), dev)
+    pv = _PILOTS.get(pvals, dev)
     H = torch.empty((f, n, cfg.fft_len), dtype=torch.complex64, device=dev) if want_h else None
     num = torch.empty((f, n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
     den = torch.empty((f, cfg.fft_len), dtype=torch.float32, device=dev)

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "paper_1901_07499_b200", "csrc"))
-from gen_twiddles import PLANS, table  # noqa: E402
+from gen_twiddles import PLANS, store_table, table  # noqa: E402
 
 from oracle import ofdm_oracle as orc  # noqa: E402
 
@@ -42,6 +42,7 @@ def dit(v):
 def model_fft(x, m):
     p, g, radices = PLANS[m]
     tw = np.array([complex(c, s) for c, s in table(m)])
+    tws = np.array([complex(c, s) for c, s in store_table(m)])
     regs = [[0j] * p for _ in range(g)]
     buf = {}
     span, tw_off, prev_r = 1, 0, None
@@ -57,18 +58,21 @@ def model_fft(x, m):
                     if pi == 0:
                         val = x[idx]
                     else:
-                        val = buf[idx + (idx >> int(math.log2(prev_r)))]
+                        val = buf[idx + 2 * (idx >> int(math.log2(prev_r)))]
                     regs[t][vv * r + brev(q, logr)] = val
-        if span > 1:
+        if pi >= 2:
             for t in range(g):
                 for vv in range(nb):
                     k = (t + vv * g) & (span - 1)
                     for q in range(1, r):
-                        regs[t][vv * r + brev(q, logr)] *= tw[tw_off + (q - 1) * span + k]
-            tw_off += (r - 1) * span
+                        regs[t][vv * r + brev(q, logr)] *= tw[(q - 1) * span + k]
         for t in range(g):
             for vv in range(nb):
                 regs[t][vv * r:(vv + 1) * r] = dit(regs[t][vv * r:(vv + 1) * r])
+        if pi == 0 and not last:
+            for t in range(g):
+                for rr in range(r):
+                    regs[t][rr] *= tws[((rr // 2) * g + t) * 2 + (rr % 2)]
         if not last:
             buf = {}
             for t in range(g):
@@ -77,7 +81,7 @@ def model_fft(x, m):
                     base = (b // span) * span * r + (b & (span - 1))
                     for rr in range(r):
                         o = base + rr * span
-                        buf[o + (o >> logr)] = regs[t][vv * r + rr]
+                        buf[o + 2 * (o >> logr)] = regs[t][vv * r + rr]
             assert len(buf) == m
         prev_r = r
         span *= r
@@ -101,18 +105,19 @@ def test_plan_model_matches_shifted_dft(m):
 
 @pytest.mark.parametrize("m", sorted(PLANS))
 def test_exchange_pad_is_bank_friendly(m):
-    """Pass-0 stores of a warp (up to 32 consecutive lane threads, fixed r)
-    hit each 4-byte bank at most twice (= 2 wavefronts for 256 B)."""
+    """Pass-0 128-bit stores of (r, r+1) pairs: each quarter-warp phase (8 lane
+    threads) covers 32 distinct banks, and the pairs are 16-B aligned."""
     p, g, radices = PLANS[m]
     if len(radices) == 1:
         return
     r = radices[0]
     logr = int(math.log2(r))
-    for rr in range(r):
-        banks = {}
-        for t in range(min(g, 32)):
-            o = t * r + rr  # span 1 => base = b * r
-            w = 2 * (o + (o >> logr))
-            for word in (w, w + 1):
-                banks.setdefault(word % 32, set()).add(word)
-        assert max(len(s) for s in banks.values()) <= 2
+    for rr in range(0, r, 2):
+        for phase in range(0, min(g, 32), 8):
+            banks = []
+            for t in range(phase, min(phase + 8, g)):
+                o = t * r + rr
+                e = o + 2 * (o >> logr)
+                assert e % 2 == 0
+                banks += [(2 * e + w) % 32 for w in range(4)]
+            assert len(banks) == len(set(banks))
