@@ -36,10 +36,21 @@ struct FusedCfg {
   static constexpr int HSTRIDE = M + 2;       // one item's H block in a ring slot (float2)
   static constexpr int RING = 2;  // must be a multiple of the pilot-unit count (1 or 2)
   static constexpr int NSTAGE = M >= 4096 ? 1 : 2;
+  // mbarriers + the TMEM base-address word, rounded up to 128 B
+  __host__ __device__ static size_t bar_bytes(int lanes, int ngroups) {
+    return ((size_t)(NSTAGE * lanes + 2 * ngroups * RING + 1) * 8 + 127) & ~size_t(127);
+  }
   static size_t smem_bytes(int ngroups, int per_group) {
     const int units = ngroups * per_group, lanes = units * GI;
-    const size_t bars = ((size_t)(NSTAGE * lanes + 2 * ngroups * RING) * 8 + 127) & ~size_t(127);
-    return bars + (size_t)NSTAGE * lanes * SLOT_STRIDE * 8 + (size_t)ngroups * RING * GI * HSTRIDE * 8;
+    return bar_bytes(lanes, ngroups) + (size_t)NSTAGE * lanes * SLOT_STRIDE * 8 +
+           (size_t)ngroups * RING * GI * HSTRIDE * 8;
+  }
+  // TMEM columns: warps of a lane quarter (warp % 4) stack 2P columns each
+  __host__ __device__ static uint32_t tmem_cols(int nwarps) {
+    const uint32_t need = (uint32_t)((nwarps + 3) / 4) * 2 * PI::P;
+    uint32_t c = 32;
+    while (c < need) c <<= 1;
+    return c;
   }
 };
 
@@ -53,6 +64,10 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
   using FC = FusedCfg<M>;
   constexpr int P = PI::P, G = PI::G, UT = FC::UT, GI = FC::GI, RING = FC::RING, NSTAGE = FC::NSTAGE;
   constexpr int SS = FC::SLOT_STRIDE, HS = FC::HSTRIDE;
+  // MRC accumulators (re, im per point; den for pilots) live in TMEM between
+  // antenna steps, keeping the FFT's register budget free for twiddle prefetch
+  constexpr bool USE_TMEM = P >= 8;
+  constexpr int NACC = 2 * P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
   const int npilot = p.npilot;          // pilot units per group (alternate antennas)
@@ -62,7 +77,8 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
   uint64_t* tma_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [NSTAGE][lanes]
   uint64_t* full_bar = tma_bar + NSTAGE * lanes;               // [ngroups][RING]
   uint64_t* empty_bar = full_bar + ngroups * RING;             // [ngroups][RING]
-  const size_t bar_bytes = ((size_t)(NSTAGE * lanes + 2 * ngroups * RING) * 8 + 127) & ~size_t(127);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty_bar + ngroups * RING);
+  const size_t bar_bytes = FC::bar_bytes(lanes, ngroups);
   float2* slots = reinterpret_cast<float2*>(smem_raw + bar_bytes);  // [NSTAGE][lanes][SS]
   float2* ring = slots + (size_t)NSTAGE * lanes * SS;               // [ngroups][RING][GI][HS]
 
@@ -73,6 +89,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
   const int sub = u / G;
   const int t = u - sub * G;
   const int lane = unit * GI + sub;
+  const int warp = threadIdx.x >> 5;
   const int work = blockIdx.x * p.fpb + grp * GI + sub;
   const bool item_ok = work < p.n_work;
   const int f = item_ok ? work / p.n_chunks : 0;
@@ -101,7 +118,18 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
     }
     fence_mbar_init();
   }
+  const int nwarps = blockDim.x >> 5;
+  const uint32_t tmem_cols = FC::tmem_cols(nwarps);
+  if constexpr (USE_TMEM) {
+    if (warp == 0) tmem_alloc(tmem_slot, tmem_cols);
+    tmem_fence_before();
+  }
   __syncthreads();
+  uint32_t tacc = 0;
+  if constexpr (USE_TMEM) {
+    tmem_fence_after();
+    tacc = *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * NACC);
+  }
 
   const bool leader = active && t == 0;
   uint64_t pol = 0;
@@ -124,11 +152,34 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
     for (int i = 0; i < P; ++i) pmask |= (__ldg(p.pilot + shifted_bin<M>(i, t)).x < 0.0f ? 1u : 0u) << i;
   }
 
+  // accumulator storage: TMEM columns of this warp, or registers for tiny P
+  float accr[USE_TMEM ? 1 : NACC];
+  auto acc_load = [&](float* a) {
+    if constexpr (USE_TMEM) {
+      tmem_wait_st();
+      tmem_ld<NACC>(tacc, a);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int i = 0; i < NACC; ++i) a[i] = accr[i];
+    }
+  };
+  auto acc_store = [&](const float* a) {
+    if constexpr (USE_TMEM) tmem_st<NACC>(tacc, a);
+    else {
+#pragma unroll
+      for (int i = 0; i < NACC; ++i) accr[i] = a[i];
+    }
+  };
+  {
+    float z[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) z[i] = 0.0f;
+    acc_store(z);
+  }
+
   const bool write_h = is_pilot && active && chunk == 0 && p.H != nullptr;
   float2 v[P];
-  float2 acc[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) acc[i] = make_float2(0.0f, 0.0f);
   float2* hring_grp = ring + (size_t)grp * RING * GI * HS + (size_t)sub * HS;
 
   for (int k = 0, n = n_first; n < p.n_ant; ++k, n += n_step) {
@@ -146,30 +197,37 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
     const int r = n % RING;
     const int j = n / RING;
     float2* hb = hring_grp + (size_t)r * GI * HS;
+    float a[NACC];
     if (is_pilot) {
       if constexpr (BPSK) asm volatile("" : "+r"(pmask));  // keep the per-bit sign words out of registers
       if (p.dc > 0) mbar_wait_parity(&empty_bar[grp * RING + r], (j + 1) & 1);  // data units done with H_{n-RING}
 #pragma unroll
-      for (int i = 0; i < P; i += 2) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float2 y = v[i + e];
-          float2 h;
-          if constexpr (BPSK) {
-            const uint32_t sgn = (pmask << (31 - (i + e))) & 0x80000000u;
-            h = make_float2(__uint_as_float(__float_as_uint(y.x) ^ sgn), __uint_as_float(__float_as_uint(y.y) ^ sgn));
-          } else {
-            // H = Y / P for unit-modulus P == Y * conj(P)
-            const float2 pc = __ldg(p.pilot + shifted_bin<M>(i + e, t));
-            h = make_float2(fmaf(y.y, pc.y, y.x * pc.x), fmaf(-y.x, pc.y, y.y * pc.x));
-          }
-          acc[i + e].x = fmaf(h.x, h.x, fmaf(h.y, h.y, acc[i + e].x));
-          v[i + e] = h;
+      for (int i = 0; i < P; ++i) {
+        const float2 y = v[i];
+        float2 h;
+        if constexpr (BPSK) {
+          const uint32_t sgn = (pmask << (31 - i)) & 0x80000000u;
+          h = make_float2(__uint_as_float(__float_as_uint(y.x) ^ sgn), __uint_as_float(__float_as_uint(y.y) ^ sgn));
+        } else {
+          // H = Y / P for unit-modulus P == Y * conj(P)
+          const float2 pc = __ldg(p.pilot + shifted_bin<M>(i, t));
+          h = make_float2(fmaf(y.y, pc.y, y.x * pc.x), fmaf(-y.x, pc.y, y.y * pc.x));
         }
-        *reinterpret_cast<float4*>(hb + (i >> 1) * 2 * G + 2 * t) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
+        v[i] = h;
       }
+#pragma unroll
+      for (int i = 0; i < P; i += 2)
+        *reinterpret_cast<float4*>(hb + (i >> 1) * 2 * G + 2 * t) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
       unit_sync();
       if (u == 0) mbar_arrive(&full_bar[grp * RING + r]);
+      acc_load(a);
+#pragma unroll
+      for (int i = 0; i < P; ++i) {  // (sum h.x^2, sum h.y^2) per subcarrier, added at the end
+        const float2 d2 = upk(fma2(pk(v[i]), pk(v[i]), pk(a[2 * i], a[2 * i + 1])));
+        a[2 * i] = d2.x;
+        a[2 * i + 1] = d2.y;
+      }
+      acc_store(a);
       if (write_h) {  // off the critical path: the data units already have H_n
         float2* hdst = p.H + ((long long)f * p.n_ant + n) * M + t;
 #pragma unroll
@@ -177,6 +235,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
       }
     } else {
       mbar_wait_parity(&full_bar[grp * RING + r], j & 1);
+      acc_load(a);
 #pragma unroll
       for (int i = 0; i < P; i += 2) {
         const float4 hh = *reinterpret_cast<const float4*>(hb + (i >> 1) * 2 * G + 2 * t);
@@ -184,9 +243,11 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const float2 y = v[i + e];
-          // conj(H) * Y, expanded as in numba_backend.py:149-150
-          acc[i + e].x = fmaf(h[e].y, y.y, fmaf(h[e].x, y.x, acc[i + e].x));
-          acc[i + e].y = fmaf(-h[e].y, y.x, fmaf(h[e].x, y.y, acc[i + e].y));
+          // conj(H) * Y = h.x * (y.x, y.y) + h.y * (y.y, -y.x)  (numba_backend.py:149-150)
+          const float2 m = upk(fma2(bc(h[e].y), pk(y.y, -y.x),
+                                    fma2(bc(h[e].x), pk(y), pk(a[2 * (i + e)], a[2 * (i + e) + 1]))));
+          a[2 * (i + e)] = m.x;
+          a[2 * (i + e) + 1] = m.y;
           if constexpr (ZF) {
             if (active) {
               const float dn = fmaxf(fmaf(h[e].x, h[e].x, h[e].y * h[e].y), p.eps);
@@ -199,36 +260,44 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
       }
       unit_sync();
       if (u == 0) mbar_arrive(&empty_bar[grp * RING + r]);
+      acc_store(a);
     }
   }
 
   // ---- epilogue: combine the pilots' den partials, divide, demap ----------
-  __syncthreads();  // ring traffic finished
+  float a[NACC];
+  acc_load(a);  // every unit: its accumulators back to registers
+  if constexpr (USE_TMEM) tmem_fence_before();
+  __syncthreads();  // ring traffic finished; TMEM reads done
+  if constexpr (USE_TMEM) {
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tmem_slot, tmem_cols);
+  }
   uint32_t flag = 0;
   // den partial of pilot unit q lives in ring slot q of this item
   if (is_pilot) {
     float* dpart = reinterpret_cast<float*>(hring_grp + (size_t)sl * GI * HS);
 #pragma unroll
-    for (int i = 0; i < P; ++i) dpart[i * G + t] = acc[i].x;
+    for (int i = 0; i < P; ++i) dpart[i * G + t] = a[2 * i] + a[2 * i + 1];
   }
   __syncthreads();
   float* dslot = reinterpret_cast<float*>(hring_grp);
+  float den[P];
   if (sl == 0) {
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-      float den = dslot[i * G + t];
-      for (int q = 1; q < npilot; ++q) den += reinterpret_cast<const float*>(hring_grp + (size_t)q * GI * HS)[i * G + t];
-      acc[i].x = den;
+      den[i] = dslot[i * G + t];
+      for (int q = 1; q < npilot; ++q) den[i] += reinterpret_cast<const float*>(hring_grp + (size_t)q * GI * HS)[i * G + t];
     }
   }
   __syncthreads();
   if (sl == 0) {
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-      dslot[i * G + t] = acc[i].x;
+      dslot[i * G + t] = den[i];
       if (active) {
-        if (!isfinite(acc[i].x)) flag |= 1u;
-        if (acc[i].x < p.eps) flag |= 2u;
+        if (!isfinite(den[i])) flag |= 1u;
+        if (den[i] < p.eps) flag |= 2u;
       }
     }
     if (active && chunk == 0) {
@@ -236,7 +305,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
       if (wdst != nullptr) {
         float* w = wdst + (long long)f * M + t;
 #pragma unroll
-        for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = acc[i].x;
+        for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = den[i];
       }
     }
   }
@@ -250,7 +319,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const float dd = fmaxf(dslot[i * G + t], p.eps);  // np.maximum(den, eps)
-        const float2 sh = make_float2(acc[i].x / dd, acc[i].y / dd);
+        const float2 sh = make_float2(a[2 * i] / dd, a[2 * i + 1] / dd);
         if (!isfinite(sh.x) || !isfinite(sh.y)) flag |= 1u;
         const int j = shifted_bin<M>(i, 0);
         sdst[j] = sh;
@@ -260,8 +329,8 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(c
       float2* ndst = p.part_num + sym_base + t;
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        if (!isfinite(acc[i].x) || !isfinite(acc[i].y)) flag |= 1u;
-        ndst[shifted_bin<M>(i, 0)] = acc[i];
+        if (!isfinite(a[2 * i]) || !isfinite(a[2 * i + 1])) flag |= 1u;
+        ndst[shifted_bin<M>(i, 0)] = make_float2(a[2 * i], a[2 * i + 1]);
       }
     }
   }
