@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -288,8 +288,21 @@ def run_b200(args, cfg_name, world, rank, local):
     out = frames.allocate_outputs(F, n, m, d, qam, dev)
     stream = torch.cuda.current_stream()
 
+    sharded = None
+    if cfg_name == "C4" and world > 1:
+        # antenna-sharded MRC: every rank holds N/world antennas of the same frames
+        from paper_1901_07499_b200 import sharding
+
+        sharded = sharding.AntennaShardedReceiver(cfg, d, symbol0_offset=s0, mode=args.exchange)
+        x = x[:, sharded.ant_lo:sharded.ant_hi].contiguous()
+
     def step():
-        frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out)
+        if sharded is not None:
+            s_hat, w, bits, fl, _ = sharded.receive(x)
+            out.bits.copy_(bits)
+            out.flags.copy_(fl)
+        else:
+            frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out)
 
     # correctness spot-check of the benchmarked configuration (bits vs truth)
     step()
@@ -318,16 +331,21 @@ def run_b200(args, cfg_name, world, rank, local):
     total_ms = t_start.elapsed_time(t_stop)
     kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     ms_step = allreduce_max(world, total_ms / args.steps)
-    value = world * F * (1 + d) / (ms_step * 1e-3)
+    # frame sharding: every rank owns F distinct frames; antenna sharding: all
+    # ranks cooperate on the same F frames
+    value = (1 if sharded is not None else world) * F * (1 + d) / (ms_step * 1e-3)
 
     peak, peak_kind = load_peaks()
-    bpf = frame_bytes(n, m, qam, d)
+    bpf = frame_bytes(n // (world if sharded is not None else 1), m, qam, d)
     achieved = bpf * F / (kernel_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg_name}.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get("bytes_per_launch")
+            tj = json.load(fh)
+        traffic = tj["dram_bytes_per_frame"] * F / (kernel_ms * 1e-3) / 1e9 if "dram_bytes_per_frame" in tj else None
+        traffic = {"dram_bytes_per_launch": int(tj["dram_bytes_per_frame"] * F), "as_gbs": traffic,
+                   "source": tj.get("source")} if traffic else None
 
     line = {
         "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
@@ -336,7 +354,8 @@ def run_b200(args, cfg_name, world, rank, local):
         "data": "synthetic: reference TX (PN|pilot|data, Gray QAM) through flat Rayleigh at 10 dB; "
                 f"{DISTINCT} distinct frames tiled on device",
         "config": {"workload": f"{cfg_name}: {n} ant x FFT {m} (CP {cp}), {qam}-QAM, 1 pilot + {d} data symbols/frame",
-                   "frames_per_gpu": F, "global_frames": F * world, "parallelism": f"frame-sharded x{world}",
+                   "frames_per_gpu": F, "global_frames": F * world, "parallelism": (f"antenna-sharded x{world} ({args.exchange} exchange of MRC partials over NCCL)"
+                                   if sharded is not None else f"frame-sharded x{world}"),
                    "input_bytes_per_gpu": int(x.numel() * 8), "l2": "inputs 6.3 GB/GPU > L2, no flush needed"
                    if x.numel() * 8 > 126e6 else "inputs smaller than L2"},
         "gpu_launches": args.steps,
@@ -349,6 +368,8 @@ def run_b200(args, cfg_name, world, rank, local):
     }
     if args.e2e_frames > 0:
         line["e2e"] = run_e2e(args, cfg, x, s0, d, world)
+    if not args.no_stages and world == 1 and cfg_name != "C4":
+        line["stages"] = run_stages(args, cfg, x, s0, d)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_port_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds)
     return line
@@ -356,7 +377,8 @@ def run_b200(args, cfg_name, world, rank, local):
 
 def run_e2e(args, cfg, x_dev, s0, d, world):
     """Same metric through the public API from pinned host memory: every step
-    copies its frames H2D, runs receive_frames, and reads the bits back."""
+    streams its frames H2D (chunked, overlapped with the fused kernel and the
+    D2H of the bits via frames.StreamingReceiver) and reads the bits back."""
     import torch
 
     from paper_1901_07499_b200 import frames
@@ -365,30 +387,67 @@ def run_e2e(args, cfg, x_dev, s0, d, world):
     host = torch.empty((Fe,) + tuple(x_dev.shape[1:]), dtype=torch.complex64, pin_memory=True)
     host.copy_(x_dev[:Fe].cpu())
     bits_host = torch.empty((Fe, d * cfg.fft_len * cfg.bits_per_qam_symbol), dtype=torch.uint8, pin_memory=True)
-    rx = frames.StreamingReceiver(cfg, Fe, symbol0_offset=s0, n_data=d) if hasattr(frames, "StreamingReceiver") else None
-
-    def step():
-        if rx is not None:
-            rx.run(host, bits_host)
-        else:
-            out = frames.receive_frames(host, cfg, symbol0_offset=s0, n_data=d, want_h=False)
-            bits_host.copy_(out.bits, non_blocking=True)
-
+    rx = frames.StreamingReceiver(cfg, min(args.e2e_chunk, Fe), d, symbol0_offset=s0,
+                                  samples_per_row=x_dev.shape[2])
     for _ in range(args.warmup):
-        step()
+        rx.run(host, bits_host)
     torch.cuda.synchronize()
     barrier(world)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
-    b.record()
+        rx.run(host, bits_host)
     torch.cuda.synchronize()
-    ms = allreduce_max(world, a.elapsed_time(b) / args.steps)
+    ms = allreduce_max(world, (time.perf_counter() - t0) * 1e3 / args.steps)
     return {"value": world * Fe * (1 + d) / (ms * 1e-3), "unit": "symbols/s",
             "h2d_bytes_per_step": int(host.numel() * 8), "d2h_bytes_per_step": int(bits_host.numel()),
-            "frames_per_step": Fe, "ms_per_step": ms,
-            "path": "pinned host -> receive_frames (public API) -> bits to pinned host"}
+            "frames_per_step": Fe, "ms_per_step": ms, "chunk_frames": min(args.e2e_chunk, Fe),
+            "path": "pinned host cf32 -> frames.StreamingReceiver (H2D | fused kernel | D2H bits on 3 streams) "
+                    "-> pinned host bits; host-timed around whole steps (includes sync)"}
+
+
+def run_stages(args, cfg, x_dev, s0, d):
+    """Per-stage µs/symbol through the staged kernels (the reference's
+    StageTimings split: fft incl. CP drop + shift, ls, mrc, demap), CUDA
+    events on F_s frames; plus the fused kernel on the same frames."""
+    import torch
+
+    from paper_1901_07499_b200 import device as dv
+    from paper_1901_07499_b200 import frames
+
+    Fs = min(args.stage_frames, x_dev.shape[0])
+    x = x_dev[:Fs]
+    n, m = cfg.n_antennas, cfg.fft_len
+    pv = torch.from_numpy(np.ascontiguousarray(
+        __import__("paper_1901_07499_b200").make_pilot(m).values, dtype=np.complex64)).cuda()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    res = {}
+
+    def timed(fn, reps=5):
+        fn()
+        a, b = ev(), ev()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(reps):
+            out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps * 1e3, out  # µs
+
+    t_fft, Y = timed(lambda: frames.fft_symbols(x, cfg, symbol0_offset=s0, n_data=d))
+    t_ls, H = timed(lambda: dv.ls(Y[:, 0], pv))
+    t_mrc, (sh, _w) = timed(lambda: dv.mrc(Y[:, 1:], H))
+    t_dm, _ = timed(lambda: dv.demap(sh.reshape(-1), cfg.qam_order))
+    out = frames.allocate_outputs(Fs, n, m, d, cfg.qam_order, x.device)
+    t_fused, _ = timed(lambda: frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out))
+    del Y, H
+    res = {"frames": Fs,
+           "fft_us_per_symbol": t_fft / (Fs * (1 + d)),
+           "ls_us_per_pilot_symbol": t_ls / Fs,
+           "mrc_us_per_data_symbol": t_mrc / (Fs * d),
+           "demap_us_per_data_symbol": t_dm / (Fs * d),
+           "fused_us_per_symbol": t_fused / (Fs * (1 + d)),
+           "note": "staged kernels write every intermediate (Y, H) to HBM; the fused kernel keeps them on chip"}
+    return res
 
 
 def main():
@@ -399,9 +458,13 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default per config)")
-    ap.add_argument("--e2e-frames", type=int, default=64)
+    ap.add_argument("--e2e-frames", type=int, default=128)
+    ap.add_argument("--e2e-chunk", type=int, default=16)
+    ap.add_argument("--stage-frames", type=int, default=64)
+    ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="gather", choices=["gather", "allreduce"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -120,7 +120,11 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     if out is None:
         out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
     else:
-        out.flags.zero_()
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                out.flags.zero_()
+        else:
+            out.flags.zero_()
     _lib.call("ofdmrx_rx_frames", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(out.H),
               device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
               device.ptr(out.flags), device.stream_handle(stream))
@@ -191,3 +195,66 @@ def fft_symbols(rx, cfg, *, symbol0_offset=0, n_data=None, first_symbol=0, n_sym
     _lib.call("ofdmrx_fft_shift", ctypes.byref(desc), int(first_symbol), int(n_symbols), device.ptr(x),
               device.ptr(y), device.stream_handle(stream))
     return y
+
+
+class StreamingReceiver:
+    """Pipelined host-to-host receive through the public API (SURVEY.md §8(f)
+    #2: the paper's bottleneck was the CPU<->GPU transfer).
+
+    Frames stream from pinned host memory in chunks: chunk i+1's H2D copy (copy
+    stream) overlaps chunk i's fused kernel (compute stream) and chunk i-1's
+    D2H of bits (+ optionally s_hat) on a third stream.  Double-buffered device
+    staging; `run` blocks until every result is back in host memory."""
+
+    def __init__(self, cfg, chunk_frames, n_data, symbol0_offset=0, samples_per_row=None, pilot=None,
+                 copy_s_hat=False, device_index=None):
+        self.cfg = cfg
+        self.fc = int(chunk_frames)
+        self.n_data = int(n_data)
+        self.s0 = int(symbol0_offset)
+        self.samples = int(samples_per_row or symbol0_offset + (1 + n_data) * cfg.symbol_len)
+        self.pilot = pilot
+        self.copy_s_hat = copy_s_hat
+        self.dev = device.require_cuda(None if device_index is None else f"cuda:{device_index}")
+        shape = (self.fc, cfg.n_antennas, self.samples)
+        self.x = [torch.empty(shape, dtype=torch.complex64, device=self.dev) for _ in range(2)]
+        self.out = [allocate_outputs(self.fc, cfg.n_antennas, cfg.fft_len, self.n_data, cfg.qam_order, self.dev,
+                                     want_h=False) for _ in range(2)]
+        self.s_h2d = torch.cuda.Stream(self.dev)
+        self.s_comp = torch.cuda.Stream(self.dev)
+        self.s_d2h = torch.cuda.Stream(self.dev)
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_done = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+
+    def run(self, host_rx, host_bits, host_s_hat=None):
+        """host_rx: pinned complex64 [F, N, S]; host_bits: pinned uint8 [F, D*M*b]."""
+        F = host_rx.shape[0]
+        n_chunks = (F + self.fc - 1) // self.fc
+        for c in range(n_chunks):
+            b = c & 1
+            lo, hi = c * self.fc, min(F, (c + 1) * self.fc)
+            n = hi - lo
+            with torch.cuda.stream(self.s_h2d):
+                if c >= 2:
+                    self.s_h2d.wait_event(self.ev_done[b])  # kernel of chunk c-2 done with x[b]
+                self.x[b][:n].copy_(host_rx[lo:hi], non_blocking=True)
+                self.ev_in[b].record(self.s_h2d)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(self.ev_in[b])
+                if c >= 2:
+                    self.s_comp.wait_event(self.ev_out[b])  # D2H of chunk c-2 done with out[b]
+                receive_frames(self.x[b][:n], self.cfg, self.pilot, symbol0_offset=self.s0, n_data=self.n_data,
+                               out=_slice_batch(self.out[b], n), stream=self.s_comp)
+                self.ev_done[b].record(self.s_comp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(self.ev_done[b])
+                host_bits[lo:hi].copy_(self.out[b].bits[:n], non_blocking=True)
+                if host_s_hat is not None:
+                    host_s_hat[lo:hi].copy_(self.out[b].s_hat[:n], non_blocking=True)
+                self.ev_out[b].record(self.s_d2h)
+        self.s_d2h.synchronize()
+
+
+def _slice_batch(out, n):
+    return FrameBatch(H=None, s_hat=out.s_hat[:n], weights=out.weights[:n], bits=out.bits[:n], flags=out.flags[:n])

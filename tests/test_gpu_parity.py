@@ -274,3 +274,47 @@ def test_large_batch_properties(P):
     assert np.array_equal(bits.reshape(32, 8, -1), np.broadcast_to(bits[:8], (32,) + bits[:8].shape))
     ber = np.mean(bits[:8] != np.stack(tx_bits))
     assert ber < 1e-3
+
+
+@pytest.mark.parametrize("mode", ["gather", "allreduce"])
+def test_antenna_sharded_receiver_world1(P, mode):
+    """AntennaShardedReceiver through torch.distributed (NCCL, world size 1)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1901_07499_b200 import sharding
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        m, cp, n_ant, qam, d = 512, 64, 16, 64, 5
+        cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+        streams, _, s0 = make_batch(m, cp, n_ant, qam, d, (71, 72))
+        x = torch.from_numpy(streams.astype(np.complex64)).cuda()
+        rx = sharding.AntennaShardedReceiver(cfg, d, symbol0_offset=s0, mode=mode)
+        s_hat, w, bits, fl, _ = rx.receive(x)
+        for i, (H, s_ref, w_ref, b_ref) in enumerate(oracle_frames(streams, s0, m, cp, d, qam)):
+            assert np.array_equal(bits[i].cpu().numpy(), b_ref)
+            assert rel(s_hat[i].cpu().numpy(), s_ref) < REL_TOL
+        assert int(fl.abs().sum()) == 0
+    finally:
+        dist.destroy_process_group()
+
+
+def test_streaming_receiver_matches_batch(P):
+    from paper_1901_07499_b200 import frames
+
+    m, cp, n_ant, qam, d = 256, 32, 16, 16, 10
+    cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    streams, _, s0 = make_batch(m, cp, n_ant, qam, d, range(5))
+    host = torch.from_numpy(streams.astype(np.complex64)).pin_memory()
+    bits = torch.empty((5, d * m * 4), dtype=torch.uint8).pin_memory()
+    s_hat = torch.empty((5, d, m), dtype=torch.complex64).pin_memory()
+    rx = frames.StreamingReceiver(cfg, 2, d, symbol0_offset=s0, samples_per_row=streams.shape[2])
+    rx.run(host, bits, s_hat)
+    for i, (H, s_ref, w_ref, b_ref) in enumerate(oracle_frames(streams, s0, m, cp, d, qam)):
+        assert np.array_equal(bits[i].numpy(), b_ref)
+        assert rel(s_hat[i].numpy(), s_ref) < REL_TOL
