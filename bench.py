@@ -434,12 +434,13 @@ def run_stages(args, cfg, x_dev, s0, d):
         return a.elapsed_time(b) / reps * 1e3, out  # µs
 
     t_fft, Y = timed(lambda: frames.fft_symbols(x, cfg, symbol0_offset=s0, n_data=d))
-    t_ls, H = timed(lambda: dv.ls(Y[:, 0], pv))
-    t_mrc, (sh, _w) = timed(lambda: dv.mrc(Y[:, 1:], H))
+    Yp, Yd = Y[:, 0].contiguous(), Y[:, 1:].contiguous()
+    t_ls, H = timed(lambda: dv.ls(Yp, pv))
+    t_mrc, (sh, _w) = timed(lambda: dv.mrc(Yd, H))
     t_dm, _ = timed(lambda: dv.demap(sh.reshape(-1), cfg.qam_order))
     out = frames.allocate_outputs(Fs, n, m, d, cfg.qam_order, x.device)
     t_fused, _ = timed(lambda: frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out))
-    del Y, H
+    del Y, Yp, Yd, H
     res = {"frames": Fs,
            "fft_us_per_symbol": t_fft / (Fs * (1 + d)),
            "ls_us_per_pilot_symbol": t_ls / Fs,
@@ -448,6 +449,96 @@ def run_stages(args, cfg, x_dev, s0, d):
            "fused_us_per_symbol": t_fused / (Fs * (1 + d)),
            "note": "staged kernels write every intermediate (Y, H) to HBM; the fused kernel keeps them on chip"}
     return res
+
+
+# ---------------------------------------------------------------------------
+# C5 sweep: antennas x FFT size, per-stage timing vs the reference CPU path,
+# written in the reference bench CSV schema (ofdmrx/bench.py:22-24)
+# ---------------------------------------------------------------------------
+
+CSV_HEADER = "fft_len,cp_len,n_antennas,engine,workers,phase,stage,mean_us,std_us,n_symbols"
+
+
+def run_sweep(args):
+    import csv
+
+    import torch
+
+    from paper_1901_07499_b200 import synth
+    from paper_1901_07499_b200.waveform import OfdmConfig, default_cp
+
+    torch.cuda.set_device(0)
+    ants = [int(a) for a in args.sweep_antennas.split(",")]
+    ffts = [int(m) for m in args.sweep_ffts.split(",")]
+    qam, d = 16, 10
+    ref = reference_importable()
+    if ref:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ofdmrx_numba_cache")
+        from ofdmrx import receiver as rref, waveform as wref
+    rows = []
+    summary = []
+    for m in ffts:
+        cp = default_cp(m)
+        for n in ants:
+            cfg = OfdmConfig(m, cp, n, qam_order=qam)
+            rx, _, s0 = synth.synth_batch(cfg, d, range(2), snr_db=10.0)
+            F = max(2, min(4096, (1 << 26) // (n * m * (1 + d))))
+            x = torch.from_numpy(rx).cuda().repeat((F + 1) // 2, 1, 1)[:F].contiguous()
+            st = run_stages(argparse.Namespace(stage_frames=F), cfg, x, s0, d)
+            g = [("estimation", "fft", st["fft_us_per_symbol"], F),
+                 ("estimation", "ls", st["ls_us_per_pilot_symbol"], F),
+                 ("demodulation", "fft", st["fft_us_per_symbol"], F * d),
+                 ("demodulation", "mrc", st["mrc_us_per_data_symbol"] + st["demap_us_per_data_symbol"], F * d),
+                 ("demodulation", "fused", st["fused_us_per_symbol"], F * (1 + d))]
+            for phase, stage, us, ns in g:
+                rows.append((m, cp, n, "b200", 1, phase, stage, us, 0.0, ns))
+            cpu = {}
+            if ref:
+                rcfg = wref.OfdmConfig(m, cp, n, qam_order=qam)
+                pilot = wref.make_pilot(m)
+                eng = rref.SequentialEngine()
+                x0 = rx[0].astype(np.complex128)
+                sym = lambda k: x0[:, s0 + k * (m + cp): s0 + (k + 1) * (m + cp)]  # noqa: E731
+
+                def best(fn, reps=3):
+                    ts = []
+                    for _ in range(reps):
+                        t0 = time.perf_counter()
+                        out = fn()
+                        ts.append(time.perf_counter() - t0)
+                    return min(ts) * 1e6, out
+
+                best(lambda: rref.to_freq(rref.cp_drop(sym(0), rcfg), eng), 1)  # JIT
+                t_fft, Y0 = best(lambda: rref.to_freq(rref.cp_drop(sym(0), rcfg), eng))
+                t_ls, est = best(lambda: rref.ls_estimate(Y0, pilot, eng))
+                Y1 = rref.to_freq(rref.cp_drop(sym(1), rcfg), eng)
+
+                def mrc_demap():
+                    c = rref.mrc_combine(Y1, est, eng)
+                    c.bits = wref.qam_demap(c.equalized, qam)
+                    return c
+
+                t_mrc, _ = best(mrc_demap)
+                cpu = {"fft": t_fft, "ls": t_ls, "mrc": t_mrc}
+                for phase, stage, us in (("estimation", "fft", t_fft), ("estimation", "ls", t_ls),
+                                         ("demodulation", "fft", t_fft), ("demodulation", "mrc", t_mrc)):
+                    rows.append((m, cp, n, "sequential", 1, phase, stage, us, 0.0, 1))
+            summary.append({"fft_len": m, "n_antennas": n, "frames": F,
+                            "b200_us_per_symbol": {"fft": st["fft_us_per_symbol"], "ls": st["ls_us_per_pilot_symbol"],
+                                                   "mrc+demap": st["mrc_us_per_data_symbol"] + st["demap_us_per_data_symbol"],
+                                                   "fused": st["fused_us_per_symbol"]},
+                            "cpu_us_per_symbol": cpu})
+            del x
+            torch.cuda.empty_cache()
+            print(json.dumps(summary[-1]), file=sys.stderr, flush=True)
+    with open(args.sweep_csv, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(CSV_HEADER.split(","))
+        for r in rows:
+            w.writerow(r[:7] + (repr(float(r[7])), repr(float(r[8])), r[9]))
+    return {"metric": "C5 sweep: per-stage µs/symbol, b200 vs reference CPU", "csv": args.sweep_csv,
+            "configs": len(summary), "reference_cpu": bool(ref),
+            "cpu_cores_used": 1, "engine_cpu": "reference SequentialEngine (numba backend)"}
 
 
 def main():
@@ -465,9 +556,16 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="gather", choices=["gather", "allreduce"])
+    ap.add_argument("--sweep", action="store_true", help="C5: antennas x FFT per-stage sweep -> CSV")
+    ap.add_argument("--sweep-antennas", default="1,2,4,8,16,32,64,128")
+    ap.add_argument("--sweep-ffts", default="64,128,256,512,1024,2048,4096")
+    ap.add_argument("--sweep-csv", default="gpurun_out/sweep.csv")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.sweep:
+        print(json.dumps(run_sweep(args)), flush=True)
+        return
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
