@@ -59,7 +59,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 template <int M, bool ZF, bool BPSK>
-__global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, 1) rx_fused_kernel(const FusedParams p) {
+__global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTAS) rx_fused_kernel(const FusedParams p) {
   using PI = PlanInfo<M>;
   using FC = FusedCfg<M>;
   constexpr int P = PI::P, G = PI::G, UT = FC::UT, GI = FC::GI, RING = FC::RING, NSTAGE = FC::NSTAGE;
