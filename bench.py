@@ -114,14 +114,21 @@ def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # OFDMRX_DIST_BACKEND=gloo + OFDMRX_SAME_DEVICE=1 run every rank on cuda:0
+    # (single-GPU smoke test of the multi-rank code path; not a measurement)
+    backend = os.environ.get("OFDMRX_DIST_BACKEND", "nccl")
+    dev = 0 if os.environ.get("OFDMRX_SAME_DEVICE") == "1" else local
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
-    return world, rank, local
+    return world, rank, dev
 
 
 def barrier(world):
@@ -137,7 +144,8 @@ def allreduce_max(world, value):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
