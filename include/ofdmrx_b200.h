@@ -153,6 +153,19 @@ OFDMRX_API int ofdmrx_mrc(int32_t n_frames, int32_t n_data, int32_t n_antennas, 
  * Replaces waveform.qam_demap (waveform.py:179-197). */
 OFDMRX_API int ofdmrx_demap(const void* symbols, int64_t n, int32_t qam_order, uint8_t* bits, void* stream);
 
+/*
+ * Ingest: copy the symbol payloads of the captures described by desc (CP
+ * dropped, every other sample skipped) from `src` (pinned host or device
+ * memory) into a dense device buffer dst [F, N, 1+D, M] cf32, as strided 2D
+ * copies on `stream` (copy engines, no SM work).  The host side of
+ * io_formats.read_cf32 (io_formats.py:26-30) + cli._load_capture
+ * (cli.py:249-271) + extract_slots/cp_drop (receiver.py:274-291,186-193):
+ * only the samples the FFT consumes cross PCIe.  dst then reads as a capture
+ * with cp_len = 0, symbol0_offset = 0, row_stride = (1+D)*M and
+ * frame_stride = N*(1+D)*M.
+ */
+OFDMRX_API int ofdmrx_stage_symbols(const ofdmrx_frame_desc* desc, const void* src, void* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

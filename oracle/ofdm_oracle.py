@@ -363,3 +363,47 @@ def receive_frame(streams, symbol0, fft_len, cp_len, n_data, qam_order,
     if weights is None:
         weights = np.sum(H.real**2 + H.imag**2, axis=0)
     return H, s_hat, weights, bits
+
+
+# ---------------------------------------------------------------------------
+# PN packet detection (sync.py:26-44; kernels/numpy_backend.py:48-70)
+# ---------------------------------------------------------------------------
+
+DEFAULT_THRESHOLD = 0.6  # sync.py:14
+
+
+def corr_metrics(stream, chips):
+    """Normalised sliding correlation |sum chips*conj(window)| / (|chips| |window|)
+    per window position (kernels/numpy_backend.py:48-70, np.correlate + cumsum
+    energy; windows with denom <= 1e-30 score 0)."""
+    stream = np.ascontiguousarray(stream, dtype=np.complex128)
+    chips = np.asarray(chips, dtype=np.float64)
+    n, p = stream.shape[0], chips.shape[0]
+    raw = np.correlate(stream, chips.astype(np.complex128), mode="valid")
+    power = np.empty(n + 1, dtype=np.float64)
+    power[0] = 0.0
+    np.cumsum(stream.real**2 + stream.imag**2, out=power[1:])
+    win = power[p:] - power[: n - p + 1]
+    np.maximum(win, 0.0, out=win)
+    denom = np.sqrt(np.sum(chips**2)) * np.sqrt(win)
+    out = np.zeros(n - p + 1, dtype=np.float64)
+    ok = denom > 1e-30
+    out[ok] = np.abs(raw[ok]) / denom[ok]
+    return out
+
+
+def detect_packet(streams, chips, threshold=DEFAULT_THRESHOLD):
+    """sync.detect_packet (sync.py:26-44): per-antenna argmax of corr_metrics;
+    the decision uses antenna 0.  Returns (detected, frame_start,
+    symbol0_offset, peak_metric, per_antenna_peaks)."""
+    streams = np.atleast_2d(streams)
+    chips = np.asarray(chips, dtype=np.float64)
+    if streams.shape[1] < chips.shape[0]:
+        raise ValueError("stream shorter than PN")  # InputError in the reference
+    peaks = []
+    for a in range(streams.shape[0]):
+        m = corr_metrics(streams[a], chips)
+        i = int(np.argmax(m))
+        peaks.append((i, float(m[i])))
+    start, peak = peaks[0]
+    return peak >= threshold, start, start + chips.shape[0], peak, tuple(peaks)

@@ -268,6 +268,44 @@ int ofdmrx_mrc(int32_t n_frames, int32_t n_data, int32_t n_antennas, int32_t fft
   return OFDMRX_OK;
 }
 
+int ofdmrx_stage_symbols(const ofdmrx_frame_desc* desc, const void* src, void* dst, void* stream) {
+  if (int rc = check_desc_impl(desc, -1)) return rc;
+  const long long F = desc->n_frames, N = desc->n_antennas, S = 1 + desc->n_data, M = desc->fft_len;
+  if (F == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(src, "src")) return rc;
+  if (int rc = check_ptr(dst, "dst")) return rc;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t width = (size_t)M * 8, dpitch = (size_t)S * M * 8;
+  const long long sym_len = desc->fft_len + desc->cp_len;
+  // one 2D copy per symbol covers every (frame, antenna) row when the rows are
+  // uniformly spaced; otherwise one per (frame, symbol)
+  long long rows, pitch, groups;
+  if (N == 1) {
+    rows = F, pitch = desc->frame_stride, groups = 1;
+  } else if (F == 1 || desc->frame_stride == N * desc->row_stride) {
+    rows = F * N, pitch = desc->row_stride, groups = 1;
+  } else {
+    rows = N, pitch = desc->row_stride, groups = F;
+  }
+  if (rows > 1 && pitch < M) rows = 1, groups = F * N;  // overlapping rows: plain copies
+  for (long long g = 0; g < groups; ++g) {
+    // first row of group g: frame f, antenna a
+    const long long f = rows == 1 && groups == F * N ? g / N : (groups == F ? g : 0);
+    const long long a = rows == 1 && groups == F * N ? g % N : 0;
+    for (long long sy = 0; sy < S; ++sy) {
+      const char* sp = static_cast<const char*>(src) +
+                       8 * (f * desc->frame_stride + a * desc->row_stride + desc->symbol0_offset + sy * sym_len +
+                            desc->cp_len);
+      char* dp = static_cast<char*>(dst) + 8 * (((f * N + a) * S + sy) * M);
+      cudaError_t e = rows == 1 ? cudaMemcpyAsync(dp, sp, width, cudaMemcpyDefault, s)
+                                : cudaMemcpy2DAsync(dp, dpitch, sp, (size_t)pitch * 8, width, (size_t)rows,
+                                                    cudaMemcpyDefault, s);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync (stage_symbols)");
+    }
+  }
+  return OFDMRX_OK;
+}
+
 int ofdmrx_demap(const void* symbols, int64_t n, int32_t qam_order, uint8_t* bits, void* stream) {
   if (int rc = check_qam(qam_order)) return rc;
   if (n < 0) return fail(OFDMRX_ERR_CONTRACT, "n must be >= 0");

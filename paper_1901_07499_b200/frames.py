@@ -112,13 +112,18 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
         n_data = (s - symbol0_offset) // sym_len - 1
     if n_data < 0 or symbol0_offset < 0:
         raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
+    desc_args = (f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
+    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream)
+
+
+def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream):
+    f, n, _, _, n_data = desc_args[:5]
     pvals = _pilot_values(pilot, cfg.fft_len)
-    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps,
-                            options=device.pilot_options(pvals))
-    device.check_desc(desc, f * n * s)
-    pv = _PILOTS.get(pvals, dev)
+    desc = device.make_desc(*desc_args, options=device.pilot_options(pvals))
+    device.check_desc(desc, x.numel())
+    pv = _PILOTS.get(pvals, x.device)
     if out is None:
-        out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
+        out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, x.device, want_h=want_h, zf=zf)
     else:
         if stream is not None:
             with torch.cuda.stream(stream):
@@ -131,6 +136,42 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     if check:
         device.raise_on_flags(out.flags)
     return out
+
+
+def stage_symbols(src, cfg, *, symbol0_offset=0, n_data, dst=None, stream=None):
+    """Ingest: copy only the symbol payloads (CP dropped) of captures `src`
+    [F, N, S] complex64 (pinned host or CUDA) into a dense CUDA tensor
+    [F, N, 1+D, M] with strided copy-engine transfers (ofdmrx_stage_symbols).
+    This is extract_slots + cp_drop (receiver.py:274-291,186-193) applied
+    before the bytes cross PCIe."""
+    if src.dim() == 2:
+        src = src[None]
+    if src.dtype != torch.complex64 or not src.is_contiguous():
+        raise ContractError("stage_symbols needs a contiguous complex64 [F, N, S] tensor")
+    f, n, s = src.shape
+    dev = device.require_cuda(None if not src.is_cuda else src.device)
+    if dst is None:
+        dst = torch.empty((f, n, 1 + n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
+    if tuple(dst.shape) != (f, n, 1 + n_data, cfg.fft_len) or not dst.is_contiguous():
+        raise ContractError(f"dst must be contiguous [{f}, {n}, {1 + n_data}, {cfg.fft_len}]")
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s)
+    device.check_desc(desc, f * n * s)
+    _lib.call("ofdmrx_stage_symbols", ctypes.byref(desc), device.ctypes_void(src.data_ptr()), device.ptr(dst),
+              device.stream_handle(stream))
+    return dst
+
+
+def receive_staged(x, cfg, pilot=None, *, eps=device.MRC_WEIGHT_FLOOR, out=None, want_h=True, zf=False,
+                   check=False, stream=None):
+    """receive_frames on the dense [F, N, 1+D, M] layout stage_symbols writes
+    (cp_len 0, symbols back to back)."""
+    if x.dim() != 4 or x.dtype != torch.complex64 or not x.is_cuda:
+        raise ContractError("receive_staged needs a complex64 CUDA tensor [F, N, 1+D, M]")
+    f, n, sy, m = x.shape
+    if m != cfg.fft_len or n != cfg.n_antennas:
+        raise ContractError(f"staged batch {tuple(x.shape)} does not match the config")
+    desc_args = (f, n, m, 0, sy - 1, cfg.qam_order, 0, sy * m, n * sy * m, eps)
+    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream)
 
 
 def receive_partials(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
@@ -216,7 +257,7 @@ class StreamingReceiver:
         self.pilot = pilot
         self.copy_s_hat = copy_s_hat
         self.dev = device.require_cuda(None if device_index is None else f"cuda:{device_index}")
-        shape = (self.fc, cfg.n_antennas, self.samples)
+        shape = (self.fc, cfg.n_antennas, 1 + self.n_data, cfg.fft_len)  # CP never crosses PCIe
         self.x = [torch.empty(shape, dtype=torch.complex64, device=self.dev) for _ in range(2)]
         self.out = [allocate_outputs(self.fc, cfg.n_antennas, cfg.fft_len, self.n_data, cfg.qam_order, self.dev,
                                      want_h=False) for _ in range(2)]
@@ -238,14 +279,15 @@ class StreamingReceiver:
             with torch.cuda.stream(self.s_h2d):
                 if c >= 2:
                     self.s_h2d.wait_event(self.ev_done[b])  # kernel of chunk c-2 done with x[b]
-                self.x[b][:n].copy_(host_rx[lo:hi], non_blocking=True)
+                stage_symbols(host_rx[lo:hi], self.cfg, symbol0_offset=self.s0, n_data=self.n_data,
+                              dst=self.x[b][:n], stream=self.s_h2d)
                 self.ev_in[b].record(self.s_h2d)
             with torch.cuda.stream(self.s_comp):
                 self.s_comp.wait_event(self.ev_in[b])
                 if c >= 2:
                     self.s_comp.wait_event(self.ev_out[b])  # D2H of chunk c-2 done with out[b]
-                receive_frames(self.x[b][:n], self.cfg, self.pilot, symbol0_offset=self.s0, n_data=self.n_data,
-                               out=_slice_batch(self.out[b], n), stream=self.s_comp)
+                receive_staged(self.x[b][:n], self.cfg, self.pilot, out=_slice_batch(self.out[b], n),
+                               stream=self.s_comp)
                 self.ev_done[b].record(self.s_comp)
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(self.ev_done[b])
