@@ -166,6 +166,35 @@ OFDMRX_API int ofdmrx_demap(const void* symbols, int64_t n, int32_t qam_order, u
  */
 OFDMRX_API int ofdmrx_stage_symbols(const ofdmrx_frame_desc* desc, const void* src, void* dst, void* stream);
 
+/*
+ * PN packet detection (the step in front of the hot path).
+ * Rows are the (frame, antenna) sample streams of F captures: row (f, n)
+ * starts at rx + f*frame_stride + n*row_stride and holds n_samples cf32
+ * samples.  chips: [n_chips] f32 device array (the bipolar PN,
+ * waveform.generate_pn, waveform.py:77-117), 1 <= n_chips <= 8192.
+ * Errors: n_samples < n_chips -> OFDMRX_ERR_INPUT (sync.py:28-31).
+ *
+ * ofdmrx_corr_metrics replaces kernels.corr_metrics (kernels/__init__.py:45-48,
+ * numba_backend.py:55-87): metrics [F*N, n_samples - n_chips + 1] f32,
+ * metric[w] = |sum_i c[i] conj(s[w+i])| / (|c| |s[w:w+P]|), 0 where the
+ * denominator is <= 1e-30.
+ *
+ * ofdmrx_detect replaces the per-antenna loop of sync.detect_packet
+ * (sync.py:32-36): peak_index [F*N] i32 = first argmax of the metric,
+ * peak_metric [F*N] f64 = its value.  Windows within the fp32 error bound of
+ * the row maximum are re-scored in fp64, so index and value are the
+ * reference's up to the cf32 quantisation of the input.  scratch: device
+ * buffer of ofdmrx_detect_scratch_bytes() bytes, 8-byte aligned.  The
+ * threshold decision on antenna 0 (DetectionResult.detected) is host logic.
+ */
+OFDMRX_API int64_t ofdmrx_detect_scratch_bytes(int32_t n_frames, int32_t n_antennas, int64_t n_samples, int32_t n_chips);
+OFDMRX_API int ofdmrx_corr_metrics(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_samples,
+                                   int64_t row_stride, int64_t frame_stride, const float* chips, int32_t n_chips,
+                                   float* metrics, void* stream);
+OFDMRX_API int ofdmrx_detect(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_samples,
+                             int64_t row_stride, int64_t frame_stride, const float* chips, int32_t n_chips,
+                             void* scratch, int32_t* peak_index, double* peak_metric, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -407,3 +407,25 @@ def detect_packet(streams, chips, threshold=DEFAULT_THRESHOLD):
         peaks.append((i, float(m[i])))
     start, peak = peaks[0]
     return peak >= threshold, start, start + chips.shape[0], peak, tuple(peaks)
+
+
+# cases of tests/golden/make_golden.py SYNC_CASES (the reference's
+# tests/test_sync.py small frame through apply_channel with a timing offset)
+SYNC_CASES = [
+    ("clean_1000", 1, "identity", None, 1000, 0),
+    ("rayleigh20_50_4ant", 4, "flat_rayleigh", 20.0, 50, 1),
+    ("zero_db_a", 1, "flat_rayleigh", 0.0, 17, 3),
+    ("zero_db_b", 2, "flat_rayleigh", 0.0, 211, 4),
+    ("minus6db_8ant", 8, "flat_rayleigh", -6.0, 77, 5),
+    ("c3_like_64ant", 64, "flat_rayleigh", 10.0, 0, 6),
+]
+
+
+def sync_capture(n_antennas, mode, snr_db, timing_offset, rng_seed):
+    """tests/test_sync.py:10-14 small frame (64/16 QPSK, 4 data symbols from
+    default_rng(3)) through channel.apply_channel (channel.py:72-108)."""
+    bits = np.random.default_rng(3).integers(0, 2, size=4 * 64 * 2, dtype=np.uint8)
+    samples, _, _ = build_frame_samples(64, 16, 4, make_pilot(64), bits, generate_pn())
+    streams, _ = apply_channel(samples, n_antennas, mode=mode, snr_db=snr_db,
+                               timing_offset=timing_offset, rng_seed=rng_seed)
+    return streams

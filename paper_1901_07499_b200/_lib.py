@@ -67,6 +67,9 @@ SIGNATURES = {
     "ofdmrx_mrc": (ctypes.c_int, [_i32, _i32, _i32, _i32, _p, _i64, _i64, _p, _f32, _i32, _p, _p, _p, _p]),
     "ofdmrx_demap": (ctypes.c_int, [_p, _i64, _i32, _p, _p]),
     "ofdmrx_stage_symbols": (ctypes.c_int, [_DESC, _p, _p, _p]),
+    "ofdmrx_detect_scratch_bytes": (ctypes.c_int64, [_i32, _i32, _i64, _i32]),
+    "ofdmrx_corr_metrics": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _p, _i32, _p, _p]),
+    "ofdmrx_detect": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -147,9 +147,83 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   return OFDMRX_OK;
 }
 
+constexpr int kMaxChips = 8192;
+
+int sync_common(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_samples, int64_t row_stride,
+                int64_t frame_stride, const float* chips, int32_t n_chips, ofdmrx::SyncParams* p) {
+  if (n_frames < 0 || n_antennas < 1) return fail(OFDMRX_ERR_CONTRACT, "n_frames must be >= 0 and n_antennas >= 1");
+  if (n_chips < 1 || n_chips > kMaxChips)
+    return fail(OFDMRX_ERR_CONFIG, "PN length %d outside the device path's [1, %d]", n_chips, kMaxChips);
+  if (n_samples < n_chips)
+    return fail(OFDMRX_ERR_INPUT, "stream length %lld shorter than PN length %d", (long long)n_samples, n_chips);
+  if (n_samples - n_chips + 1 > 0x7fffffffLL) return fail(OFDMRX_ERR_CONFIG, "stream too long (%lld)", (long long)n_samples);
+  if (row_stride < 0 || frame_stride < 0) return fail(OFDMRX_ERR_CONTRACT, "strides must be >= 0");
+  if (n_antennas > 1 && row_stride < n_samples && row_stride != 0)
+    return fail(OFDMRX_ERR_CONTRACT, "row_stride %lld shorter than n_samples %lld", (long long)row_stride,
+                (long long)n_samples);
+  if (n_frames > 0) {
+    if (int rc = check_ptr(rx, "rx")) return rc;
+    if (int rc = check_align(rx, 8, "rx")) return rc;
+    if (int rc = check_ptr(chips, "chips")) return rc;
+  }
+  *p = ofdmrx::SyncParams{};
+  p->rx = static_cast<const float2*>(rx);
+  p->frame_stride = frame_stride;
+  p->row_stride = row_stride;
+  p->n_samples = n_samples;
+  p->n_frames = n_frames;
+  p->n_ant = n_antennas;
+  p->chips = chips;
+  p->n_chips = n_chips;
+  p->wins = n_samples - n_chips + 1;
+  return OFDMRX_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int64_t ofdmrx_detect_scratch_bytes(int32_t n_frames, int32_t n_antennas, int64_t n_samples, int32_t n_chips) {
+  if (n_frames < 0 || n_antennas < 1 || n_chips < 1 || n_samples < n_chips) return -1;
+  const long long rows = (long long)n_frames * n_antennas;
+  return rows * 8 + rows * (n_samples - n_chips + 1) * 4;
+}
+
+int ofdmrx_corr_metrics(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_samples, int64_t row_stride,
+                        int64_t frame_stride, const float* chips, int32_t n_chips, float* metrics, void* stream) {
+  ofdmrx::SyncParams p;
+  if (int rc = sync_common(rx, n_frames, n_antennas, n_samples, row_stride, frame_stride, chips, n_chips, &p))
+    return rc;
+  if (n_frames == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(metrics, "metrics")) return rc;
+  p.metrics = metrics;
+  cudaError_t e = ofdmrx::launch_corr(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "corr_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_detect(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_samples, int64_t row_stride,
+                  int64_t frame_stride, const float* chips, int32_t n_chips, void* scratch, int32_t* peak_index,
+                  double* peak_metric, void* stream) {
+  ofdmrx::SyncParams p;
+  if (int rc = sync_common(rx, n_frames, n_antennas, n_samples, row_stride, frame_stride, chips, n_chips, &p))
+    return rc;
+  if (n_frames == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(scratch, "scratch")) return rc;
+  if (int rc = check_align(scratch, 8, "scratch")) return rc;
+  if (int rc = check_ptr(peak_index, "peak_index")) return rc;
+  if (int rc = check_ptr(peak_metric, "peak_metric")) return rc;
+  const long long rows = (long long)n_frames * n_antennas;
+  p.keys = static_cast<unsigned long long*>(scratch);
+  p.metrics = reinterpret_cast<float*>(static_cast<char*>(scratch) + rows * 8);
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ofdmrx::launch_corr(p, s);
+  if (e != cudaSuccess) return cuda_fail(e, "corr_kernel launch");
+  e = ofdmrx::launch_refine(p, peak_index, peak_metric, s);
+  if (e != cudaSuccess) return cuda_fail(e, "refine_kernel launch");
+  return OFDMRX_OK;
+}
+
 
 int ofdmrx_abi_version(void) { return OFDMRX_ABI_VERSION; }
 

@@ -86,4 +86,19 @@ struct FinishParams {
 };
 cudaError_t launch_finish(const FinishParams& p, cudaStream_t s);
 
+// PN detection (sync.cu): rows = (frame, antenna) streams of n_samples.
+struct SyncParams {
+  const float2* rx;
+  long long frame_stride, row_stride, n_samples;
+  int n_frames, n_ant;
+  const float* chips;           // [n_chips] real chips (bipolar PN)
+  int n_chips;
+  long long wins;               // n_samples - n_chips + 1
+  float* metrics;               // [F*N, wins] fp32 metrics
+  unsigned long long* keys;     // [F*N] per-row (metric, first index) max key, or null
+};
+size_t sync_smem_bytes(int n_chips);
+cudaError_t launch_corr(const SyncParams& p, cudaStream_t s);
+cudaError_t launch_refine(const SyncParams& p, int32_t* peak_idx, double* peak_metric, cudaStream_t s);
+
 }  // namespace ofdmrx

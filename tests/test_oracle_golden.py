@@ -84,3 +84,33 @@ def test_frames_bit_exact(golden_dir, name):
             assert np.array_equal(H[rows].astype(np.complex64), g[f"{tag}_H_sub"])
             assert np.array_equal(s_hat.astype(np.complex64), g[f"{tag}_s_hat"])
         assert np.allclose(np.linalg.norm(H, axis=1), g[f"{tag}_H_norm"], rtol=0, atol=0)
+
+
+@pytest.fixture(scope="module")
+def sync(golden_dir):
+    return dict(np.load(os.path.join(golden_dir, "sync_vectors.npz")))
+
+
+def test_corr_metrics_bit_exact(sync):
+    assert np.array_equal(orc.corr_metrics(sync["corr_stream"], sync["corr_chips"]), sync["corr_out"])
+    emb = orc.corr_metrics(sync["emb_stream"], sync["emb_chips"])
+    assert np.array_equal(emb, sync["emb_out"])
+    assert int(np.argmax(emb)) == 300
+
+
+@pytest.mark.parametrize("case", orc.SYNC_CASES, ids=lambda c: c[0])
+def test_detect_packet_bit_exact(sync, case):
+    name = case[0]
+    streams = orc.sync_capture(*case[1:])
+    assert hashlib.sha256(streams.tobytes()).digest() == sync[f"{name}_sha256"].tobytes()
+    det, start, s0, peak, peaks = orc.detect_packet(streams, orc.generate_pn())
+    assert np.array_equal([p[0] for p in peaks], sync[f"{name}_peaks"])
+    assert np.array_equal([p[1] for p in peaks], sync[f"{name}_metrics"])
+    assert det == bool(sync[f"{name}_detected"]) and s0 == start + 255
+
+
+def test_noise_only_detection_bit_exact(sync):
+    pn = orc.generate_pn()
+    for i, row in enumerate(sync["noise_streams"]):
+        det, start, _, peak, _ = orc.detect_packet(row[None, :], pn)
+        assert start == sync["noise_peaks"][i] and peak == sync["noise_metrics"][i] and not det
