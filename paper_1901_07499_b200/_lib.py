@@ -16,6 +16,9 @@ from .errors import (
 )
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libofdmrx_b200.so")
+# developer knob for A/B kernel experiments (scripts/fused_quick.py); the
+# product always loads the in-tree build
+LIB_PATH = os.environ.get("OFDMRX_LIB", LIB_PATH)
 ABI_VERSION = 1
 
 OK, ERR_CONFIG, ERR_CONTRACT, ERR_INPUT, ERR_NUMERIC, ERR_CUDA = range(6)

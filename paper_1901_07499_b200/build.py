@@ -32,6 +32,29 @@ def _stale():
                for d in deps)
 
 
+def build_variant(name, defines, sources=None):
+    """Experiment build: libofdmrx_b200_<name>.so under build/variants with
+    extra -D flags (A/B timing via OFDMRX_LIB=...; never the product)."""
+    outdir = os.path.join(HERE, "..", "build", "variants")
+    os.makedirs(outdir, exist_ok=True)
+    lib = os.path.abspath(os.path.join(outdir, f"libofdmrx_b200_{name}.so"))
+    objs, procs = [], []
+    for src in sources or SOURCES:
+        obj = os.path.join(outdir, f"{name}_{src.replace('.cu', '.o')}")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+        objs.append(obj)
+    for cmd, p in procs:
+        out, _ = p.communicate()
+        if p.returncode:
+            sys.stderr.write(out)
+            raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
+    subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs], check=True)
+    for o in objs:
+        os.remove(o)
+    return lib
+
+
 def build(force=False, verbose=False):
     sys.path.insert(0, CSRC)
     try:
@@ -66,4 +89,8 @@ def build(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))

@@ -66,7 +66,11 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   constexpr int SS = FC::SLOT_STRIDE, HS = FC::HSTRIDE;
   // MRC accumulators (re, im per point; den for pilots) live in TMEM between
   // antenna steps, keeping the FFT's register budget free for twiddle prefetch
+#ifdef OFDMRX_EXP_NOTMEM
+  constexpr bool USE_TMEM = false;  // experiment: accumulators in registers (spills at P = 32)
+#else
   constexpr bool USE_TMEM = P >= 8;
+#endif
   constexpr int NACC = 2 * P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
@@ -143,6 +147,11 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     tma_bulk_g2s(slots + (size_t)(st * lanes + lane) * SS, reinterpret_cast<const void*>(start), bytes, bar, pol);
   };
   if (leader && n_first < p.n_ant) issue(n_first, 0);
+#ifdef OFDMRX_EXP_NOLOAD
+  constexpr bool kLoadEvery = false;  // experiment: compute-only (first antenna's row reused)
+#else
+  constexpr bool kLoadEvery = true;
+#endif
 
   // pilot units: BPSK (+-1 real) pilots reduce H = Y conj(P) to a sign flip; the
   // sign bits of this thread's P subcarriers are loaded once.
@@ -184,15 +193,20 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
 
   for (int k = 0, n = n_first; n < p.n_ant; ++k, n += n_step) {
     const int st = NSTAGE == 2 ? (k & 1) : 0;
-    if (NSTAGE == 2 && leader && n + n_step < p.n_ant) issue(n + n_step, st ^ 1);  // freed at the end of step k-1
+    if (kLoadEvery && NSTAGE == 2 && leader && n + n_step < p.n_ant) issue(n + n_step, st ^ 1);  // freed at the end of step k-1
     float2* slot = slots + (size_t)(st * lanes + lane) * SS;
-    if (active) mbar_wait_parity(&tma_bar[st * lanes + lane], NSTAGE == 2 ? ((k >> 1) & 1) : (k & 1));
+    if (active && (kLoadEvery || k == 0)) mbar_wait_parity(&tma_bar[st * lanes + lane], NSTAGE == 2 ? ((k >> 1) & 1) : (k & 1));
     const int sh = (int)((reinterpret_cast<uintptr_t>(row0 + (long long)n * p.row_stride) >> 3) & 1);
     const float2* src = slot + sh;
+#ifdef OFDMRX_EXP_NOFFT
+#pragma unroll
+    for (int i = 0; i < P; ++i) v[i] = src[i * G + t];  // experiment: skeleton without the FFT
+#else
     fft_forward<M>(v, slot, t, [&](int idx) { return src[idx]; }, unit_sync);
+#endif
     fence_proxy_async_smem();  // this thread's generic smem writes before the async-proxy refill
     unit_sync();               // every read of the slot done: it may be refilled
-    if (NSTAGE == 1 && leader && n + n_step < p.n_ant) issue(n + n_step, 0);
+    if (kLoadEvery && NSTAGE == 1 && leader && n + n_step < p.n_ant) issue(n + n_step, 0);
 
     const int r = n % RING;
     const int j = n / RING;
