@@ -93,6 +93,35 @@ int check_align(const void* p, unsigned a, const char* what) {
   return OFDMRX_OK;
 }
 
+// Antenna shards per frame for a mode-0 launch: enough work items for ~3
+// waves of CTAs on the 148 SMs, keeping >= 16 antennas per shard and an
+// even split (power-of-two shards, so the finish tree over shards is the
+// reference ReductionPlan order, numerics.py:85-106).
+int pick_shards(const ofdmrx_frame_desc* d, const ofdmrx::FusedLaunch& l) {
+  const long long ctas = ((long long)d->n_frames * l.n_chunks + l.fpb - 1) / l.fpb;
+  int s = 1;
+  if (d->n_data == 0) return 1;  // pilot-only frames: nothing to combine
+  while (ctas * s < 3 * 148 && d->n_antennas % (2 * s) == 0 && d->n_antennas / (2 * s) >= 16 && s < 64) s *= 2;
+  return s;
+}
+
+// stream-ordered scratch from the device's default pool, kept warm
+int scratch_alloc(void** ptr, size_t bytes, cudaStream_t st) {
+  static bool pool_set = false;
+  if (!pool_set) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_set = true;
+  }
+  cudaError_t e = cudaMallocAsync(ptr, bytes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (shard partials)");
+  return OFDMRX_OK;
+}
+
 int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, int mode, void* H, void* s_hat,
                  float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream) {
   if (int rc = check_desc_impl(d, -1)) return rc;
@@ -113,19 +142,29 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   ofdmrx::FusedLaunch l{};
   cudaError_t e = ofdmrx::fused_plan(d->fft_len, d->n_frames, d->n_data, &l);
   if (e != cudaSuccess) return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);
+  // Small batches of big frames (e.g. C4: 64 frames x 3 chunks on 148 SMs)
+  // leave SMs idle: split each frame's antennas into S shards on this device
+  // (partial MRC sums) and combine them with the pairwise-tree finish kernel.
+  const int shards = mode == 0 ? pick_shards(d, l) : 1;
+  if (shards > 1) {
+    if (e = ofdmrx::fused_plan(d->fft_len, d->n_frames * shards, d->n_data, &l); e != cudaSuccess)
+      return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);
+  }
   ofdmrx::FusedParams p{};
   p.rx = static_cast<const float2*>(rx);
   p.frame_stride = d->frame_stride;
   p.row_stride = d->row_stride;
   p.sym0 = d->symbol0_offset;
   p.n_frames = d->n_frames;
-  p.n_ant = d->n_antennas;
+  p.n_ant = d->n_antennas / shards;
+  p.ant_total = d->n_antennas;
+  p.n_shards = shards;
   p.cp = d->cp_len;
   p.n_data = d->n_data;
   p.dc = l.dc;
   p.n_chunks = l.n_chunks;
   p.fpb = l.fpb;
-  p.n_work = d->n_frames * l.n_chunks;
+  p.n_work = d->n_frames * l.n_chunks * shards;
   p.lanes = l.lanes;
   p.ngroups = l.ngroups;
   p.npilot = l.npilot;
@@ -142,8 +181,45 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   p.flags = flags;
   p.part_num = static_cast<float2*>(num);
   p.part_den = den;
-  e = ofdmrx::launch_fused(d->fft_len, p, l, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "rx_fused_kernel launch");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (shards == 1) {
+    e = ofdmrx::launch_fused(d->fft_len, p, l, st);
+    if (e != cudaSuccess) return cuda_fail(e, "rx_fused_kernel launch");
+    return OFDMRX_OK;
+  }
+  // sharded: partial sums into stream-ordered scratch, then finish
+  const size_t n_num = (size_t)shards * d->n_frames * d->n_data * d->fft_len;
+  const size_t n_den = (size_t)shards * d->n_frames * d->fft_len;
+  void* scratch = nullptr;
+  if (int rc = scratch_alloc(&scratch, n_num * 8 + n_den * 4, st)) return rc;
+  p.mode = 1;
+  p.s_hat = nullptr;
+  p.weights = nullptr;
+  p.bits = nullptr;
+  p.part_num = static_cast<float2*>(scratch);
+  p.part_den = reinterpret_cast<float*>(static_cast<char*>(scratch) + n_num * 8);
+  e = ofdmrx::launch_fused(d->fft_len, p, l, st);
+  if (e == cudaSuccess && d->n_data > 0) {
+    ofdmrx::FinishParams fp{};
+    fp.num = p.part_num;
+    fp.den = p.part_den;
+    fp.parts = shards;
+    fp.n_frames = d->n_frames;
+    fp.n_data = d->n_data;
+    fp.M = d->fft_len;
+    fp.eps = d->eps;
+    fp.qb = p.qb;
+    fp.levels = p.levels;
+    fp.qscale = p.qscale;
+    fp.s_hat = static_cast<float2*>(s_hat);
+    fp.weights = weights;
+    fp.bits = bits;
+    fp.flags = flags;
+    e = ofdmrx::launch_finish(fp, st);
+  }
+  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "sharded rx_fused_kernel / finish_kernel launch");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
   return OFDMRX_OK;
 }
 

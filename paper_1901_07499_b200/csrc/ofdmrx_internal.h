@@ -16,7 +16,8 @@ struct FusedParams {
   long long frame_stride;  // samples between frames
   long long row_stride;    // samples between antenna rows
   long long sym0;          // offset (samples) of the pilot symbol's CP inside a row
-  int n_frames, n_ant, cp, n_data;
+  int n_frames, n_ant, cp, n_data;   // n_ant = antennas per shard
+  int n_shards, ant_total;           // antenna shards per frame (mode 1 only when > 1)
   int dc, n_chunks, fpb, n_work, lanes, ngroups, npilot;
   const float2* pilot;     // [M] pilot values, subcarrier (shifted) order
   float eps;
@@ -31,8 +32,8 @@ struct FusedParams {
   uint8_t* bits;           // [F, D*M*qb]          (mode 0, required)
   float2* zf;              // [F, D, N, M]
   uint32_t* flags;         // [F]
-  float2* part_num;        // [F, D, M]            (mode 1, required)
-  float* part_den;         // [F, M]               (mode 1, required)
+  float2* part_num;        // [S, F, D, M]         (mode 1, required)
+  float* part_den;         // [S, F, M]            (mode 1, required)
 };
 
 struct FusedLaunch {

@@ -96,8 +96,12 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   const int warp = threadIdx.x >> 5;
   const int work = blockIdx.x * p.fpb + grp * GI + sub;
   const bool item_ok = work < p.n_work;
-  const int f = item_ok ? work / p.n_chunks : 0;
-  const int chunk = item_ok ? work - f * p.n_chunks : 0;
+  // work = (frame, chunk, antenna shard), shards innermost
+  const int shard = item_ok ? work % p.n_shards : 0;
+  const int fc = item_ok ? work / p.n_shards : 0;
+  const int f = fc / p.n_chunks;
+  const int chunk = fc - f * p.n_chunks;
+  const int ant0 = shard * p.n_ant;  // first antenna of this shard (global index)
   const bool is_pilot = sl < npilot;
   const int d = is_pilot ? 0 : chunk * p.dc + (sl - npilot);  // data-symbol index (0-based)
   const bool active = item_ok && (is_pilot || d < p.n_data);
@@ -112,7 +116,8 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     else named_bar_sync(1 + unit, UT);
   };
 
-  const float2* row0 = p.rx + (long long)f * p.frame_stride + p.sym0 + (long long)s * (M + p.cp) + p.cp;
+  const float2* row0 = p.rx + (long long)f * p.frame_stride + (long long)ant0 * p.row_stride + p.sym0 +
+                       (long long)s * (M + p.cp) + p.cp;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSTAGE * lanes; ++i) mbar_init(&tma_bar[i], 1);
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
       }
       acc_store(a);
       if (write_h) {  // off the critical path: the data units already have H_n
-        float2* hdst = p.H + ((long long)f * p.n_ant + n) * M + t;
+        float2* hdst = p.H + ((long long)f * p.ant_total + ant0 + n) * M + t;
 #pragma unroll
         for (int i = 0; i < P; ++i) hdst[shifted_bin<M>(i, 0)] = v[i];
       }
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
             if (active) {
               const float dn = fmaxf(fmaf(h[e].x, h[e].x, h[e].y * h[e].y), p.eps);
               const float zr = fmaf(h[e].x, y.x, h[e].y * y.y), zi = fmaf(h[e].x, y.y, -h[e].y * y.x);
-              p.zf[(((long long)f * p.n_data + d) * p.n_ant + n) * M + shifted_bin<M>(i + e, t)] =
+              p.zf[(((long long)f * p.n_data + d) * p.ant_total + ant0 + n) * M + shifted_bin<M>(i + e, t)] =
                   make_float2(zr / dn, zi / dn);
             }
           }
@@ -311,13 +316,13 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
       dslot[i * G + t] = den[i];
       if (active) {
         if (!isfinite(den[i])) flag |= 1u;
-        if (den[i] < p.eps) flag |= 2u;
+        if (p.mode == 0 && den[i] < p.eps) flag |= 2u;  // partial sums: erasure is decided after the combine
       }
     }
     if (active && chunk == 0) {
       float* wdst = p.mode == 0 ? p.weights : p.part_den;
       if (wdst != nullptr) {
-        float* w = wdst + (long long)f * M + t;
+        float* w = wdst + ((long long)shard * p.n_frames + f) * M + t;
 #pragma unroll
         for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = den[i];
       }
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   }
   __syncthreads();
   if (!is_pilot && active) {
-    const long long sym_base = ((long long)f * p.n_data + d) * M;
+    const long long sym_base = (((long long)shard * p.n_frames + f) * p.n_data + d) * M;
     if (p.mode == 0) {
       const QamParams q{p.qb, p.levels, p.qscale};
       float2* sdst = p.s_hat + sym_base + t;
