@@ -482,6 +482,7 @@ def run_stages(args, cfg, x_dev, s0, d, with_sync=True):
     t_fused, _ = timed(lambda: frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out))
     del Y, Yp, Yd, H
     sync = run_sync_stage(cfg, d, Fs, timed) if with_sync else None
+    synth_t = run_synth_stage(cfg, d, Fs, timed) if with_sync else None
     res = {"frames": Fs,
            "fft_us_per_symbol": t_fft / (Fs * (1 + d)),
            "ls_us_per_pilot_symbol": t_ls / Fs,
@@ -490,8 +491,20 @@ def run_stages(args, cfg, x_dev, s0, d, with_sync=True):
            "fused_us_per_symbol": t_fused / (Fs * (1 + d)),
            "note": "staged kernels write every intermediate (Y, H) to HBM; the fused kernel keeps them on chip; "
                    "every stage CUDA-graph captured and replayed 20x between CUDA events (GPU time only)",
-           "sync": sync}
+           "sync": sync, "synth": synth_t}
     return res
+
+
+def run_synth_stage(cfg, d, Fs, timed):
+    """Device frame synthesizer (synth.synth_frames: device bits, flat
+    Rayleigh, 10 dB AWGN, PN preamble) over Fs frames: µs per frame and the
+    write bandwidth of the rx it produces."""
+    from paper_1901_07499_b200 import synth
+
+    t, out = timed(lambda: synth.synth_frames(cfg, d, Fs, seed=7, snr_db=10.0))
+    nbytes = out.rx.numel() * 8
+    return {"frames": Fs, "us_per_frame": t / Fs, "rx_write_gbs": nbytes / (t * 1e-6) / 1e9,
+            "path": "ofdmrx_synth_frames: bits/gains hash RNG, tx_kernel IFFT+CP, sigpow + channel_kernel"}
 
 
 def run_sync_stage(cfg, d, Fs, timed):

@@ -195,6 +195,42 @@ OFDMRX_API int ofdmrx_detect(const void* rx, int32_t n_frames, int32_t n_antenna
                              int64_t row_stride, int64_t frame_stride, const float* chips, int32_t n_chips,
                              void* scratch, int32_t* peak_index, double* peak_metric, void* stream);
 
+/*
+ * Frame synthesizer: waveform.build_frame
+ * (waveform.py:260-286) + channel.apply_channel (channel.py:72-108) on the
+ * device.  rx row (f, n) = timing_offset noise-only samples, then
+ * conv(response[f?, n, :], PN | pilot symbol | D data symbols)[:frame_len]
+ * plus complex AWGN at snr_db below that row's mean signal power (when
+ * noisy), zero-padded/noise to n_samples.  Random draws (ofdmrx_synth_bits,
+ * ofdmrx_synth_rayleigh, the AWGN) are counter-based hashes of (seed, stream,
+ * index): reproducible, not numpy's PCG64 streams.
+ */
+typedef struct {
+  int32_t n_frames;       /* F                                             */
+  int32_t n_antennas;     /* N                                             */
+  int32_t fft_len;        /* M, power of two in [2, 4096]                  */
+  int32_t cp_len;         /* C, 0 <= C < M                                 */
+  int32_t n_data;         /* D >= 1 data symbols (bits fill them exactly)  */
+  int32_t qam_order;      /* 4, 16, 64                                     */
+  int32_t pn_len;         /* preamble chips (0 = no preamble)              */
+  int32_t n_taps;         /* response taps per antenna (1 = flat), <= 64   */
+  int32_t resp_per_frame; /* response [F,N,T] (1) or [N,T] for all frames (0) */
+  int32_t noisy;          /* 1: add AWGN at snr_db                         */
+  float snr_db;
+  int64_t timing_offset;  /* leading noise-only samples (ChannelModel.timing_offset) */
+  int64_t n_samples;      /* rx row length >= timing_offset + pn_len + (1+D)(M+C) */
+  uint64_t seed;
+} ofdmrx_synth_desc;
+
+/* bits [F, bits_per_frame] u8 0/1, fair coin per bit. */
+OFDMRX_API int ofdmrx_synth_bits(uint8_t* bits, int32_t n_frames, int64_t bits_per_frame, uint64_t seed, void* stream);
+/* resp [rows] cf32 ~ CN(0, 1): flat Rayleigh gains (channel.py:95-97). */
+OFDMRX_API int ofdmrx_synth_rayleigh(void* resp, int32_t rows, uint64_t seed, void* stream);
+/* rx [F, N, n_samples] cf32 from pilot [M] cf32, chips [pn_len] f32,
+ * bits [F, D*M*log2(Q)] u8, resp (see desc). */
+OFDMRX_API int ofdmrx_synth_frames(const ofdmrx_synth_desc* desc, const void* pilot, const float* chips,
+                                   const uint8_t* bits, const void* resp, void* rx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,30 @@ _p = ctypes.c_void_p
 _i32, _i64, _f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
 _DESC = ctypes.POINTER(FrameDesc)
 
+
+class SynthDesc(ctypes.Structure):
+    """ofdmrx_synth_desc."""
+
+    _fields_ = [
+        ("n_frames", ctypes.c_int32),
+        ("n_antennas", ctypes.c_int32),
+        ("fft_len", ctypes.c_int32),
+        ("cp_len", ctypes.c_int32),
+        ("n_data", ctypes.c_int32),
+        ("qam_order", ctypes.c_int32),
+        ("pn_len", ctypes.c_int32),
+        ("n_taps", ctypes.c_int32),
+        ("resp_per_frame", ctypes.c_int32),
+        ("noisy", ctypes.c_int32),
+        ("snr_db", ctypes.c_float),
+        ("timing_offset", ctypes.c_int64),
+        ("n_samples", ctypes.c_int64),
+        ("seed", ctypes.c_uint64),
+    ]
+
+
+_SDESC = ctypes.POINTER(SynthDesc)
+
 # exported symbol -> (restype, argtypes); must match include/ofdmrx_b200.h
 SIGNATURES = {
     "ofdmrx_abi_version": (ctypes.c_int, []),
@@ -73,6 +97,9 @@ SIGNATURES = {
     "ofdmrx_detect_scratch_bytes": (ctypes.c_int64, [_i32, _i32, _i64, _i32]),
     "ofdmrx_corr_metrics": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _p, _i32, _p, _p]),
     "ofdmrx_detect": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p]),
+    "ofdmrx_synth_bits": (ctypes.c_int, [_p, _i32, _i64, ctypes.c_uint64, _p]),
+    "ofdmrx_synth_rayleigh": (ctypes.c_int, [_p, _i32, ctypes.c_uint64, _p]),
+    "ofdmrx_synth_frames": (ctypes.c_int, [_SDESC, _p, _p, _p, _p, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -456,6 +456,83 @@ int ofdmrx_stage_symbols(const ofdmrx_frame_desc* desc, const void* src, void* d
   return OFDMRX_OK;
 }
 
+int ofdmrx_synth_bits(uint8_t* bits, int32_t n_frames, int64_t bits_per_frame, uint64_t seed, void* stream) {
+  if (n_frames < 0 || bits_per_frame < 0) return fail(OFDMRX_ERR_CONTRACT, "negative sizes");
+  if ((long long)n_frames * bits_per_frame == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(bits, "bits")) return rc;
+  cudaError_t e = ofdmrx::launch_synth_bits(bits, bits_per_frame, n_frames, seed, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "bits_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_synth_rayleigh(void* resp, int32_t rows, uint64_t seed, void* stream) {
+  if (rows < 0) return fail(OFDMRX_ERR_CONTRACT, "negative sizes");
+  if (rows == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(resp, "resp")) return rc;
+  cudaError_t e = ofdmrx::launch_synth_gains(static_cast<float2*>(resp), rows, seed, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "gains_kernel launch");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_synth_frames(const ofdmrx_synth_desc* d, const void* pilot, const float* chips, const uint8_t* bits,
+                        const void* resp, void* rx, void* stream) {
+  if (d == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
+  if (int rc = check_fft_len(d->fft_len)) return rc;
+  if (d->cp_len < 0 || d->cp_len >= d->fft_len)
+    return fail(OFDMRX_ERR_CONFIG, "cp_len must satisfy 0 <= cp_len < fft_len, got %d", d->cp_len);
+  if (int rc = check_qam(d->qam_order)) return rc;
+  if (d->n_frames < 0 || d->n_antennas < 1 || d->n_data < 1)
+    return fail(OFDMRX_ERR_CONTRACT, "need n_frames >= 0, n_antennas >= 1, n_data >= 1");
+  if (d->pn_len < 0 || d->n_taps < 1 || d->n_taps > 64 || d->timing_offset < 0)
+    return fail(OFDMRX_ERR_CONFIG, "invalid pn_len / n_taps (1..64) / timing_offset");
+  if (!std::isfinite(d->snr_db)) return fail(OFDMRX_ERR_CONFIG, "snr_db must be finite");
+  const long long tx_len = (long long)(1 + d->n_data) * (d->fft_len + d->cp_len);
+  if (d->n_samples < d->timing_offset + d->pn_len + tx_len)
+    return fail(OFDMRX_ERR_CONTRACT, "n_samples %lld < timing_offset + frame length %lld", (long long)d->n_samples,
+                (long long)(d->timing_offset + d->pn_len + tx_len));
+  if (d->n_frames == 0) return OFDMRX_OK;
+  if (int rc = check_ptr(pilot, "pilot")) return rc;
+  if (d->pn_len > 0)
+    if (int rc = check_ptr(chips, "chips")) return rc;
+  if (int rc = check_ptr(bits, "bits")) return rc;
+  if (int rc = check_ptr(resp, "resp")) return rc;
+  if (int rc = check_ptr(rx, "rx")) return rc;
+  ofdmrx::SynthParams p{};
+  p.n_frames = d->n_frames;
+  p.n_ant = d->n_antennas;
+  p.M = d->fft_len;
+  p.cp = d->cp_len;
+  p.n_data = d->n_data;
+  qam_consts(d->qam_order, &p.qb, &p.levels, &p.qscale);
+  p.pn_len = d->pn_len;
+  p.tx_len = tx_len;
+  p.n_samples = d->n_samples;
+  p.offset = d->timing_offset;
+  p.pilot = static_cast<const float2*>(pilot);
+  p.chips = chips;
+  p.bits = bits;
+  p.resp = static_cast<const float2*>(resp);
+  p.n_taps = d->n_taps;
+  p.resp_per_frame = d->resp_per_frame != 0;
+  p.noisy = d->noisy != 0;
+  p.snr_db = d->snr_db;
+  p.seed = d->seed;
+  p.rx = static_cast<float2*>(rx);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t parts = ofdmrx::synth_sig_parts(d->pn_len, tx_len);
+  const size_t tx_bytes = (size_t)d->n_frames * tx_len * 8;
+  const size_t sig_bytes = (size_t)d->n_frames * d->n_antennas * parts * 8;
+  void* scratch = nullptr;
+  if (int rc = scratch_alloc(&scratch, tx_bytes + sig_bytes, st)) return rc;
+  p.tx = static_cast<float2*>(scratch);
+  p.sig_part = reinterpret_cast<double*>(static_cast<char*>(scratch) + tx_bytes);
+  cudaError_t e = ofdmrx::launch_synth(p, st);
+  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "synth kernels launch");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
+  return OFDMRX_OK;
+}
+
 int ofdmrx_demap(const void* symbols, int64_t n, int32_t qam_order, uint8_t* bits, void* stream) {
   if (int rc = check_qam(qam_order)) return rc;
   if (n < 0) return fail(OFDMRX_ERR_CONTRACT, "n must be >= 0");

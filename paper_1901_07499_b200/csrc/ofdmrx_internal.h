@@ -102,4 +102,29 @@ size_t sync_smem_bytes(int n_chips);
 cudaError_t launch_corr(const SyncParams& p, cudaStream_t s);
 cudaError_t launch_refine(const SyncParams& p, int32_t* peak_idx, double* peak_metric, cudaStream_t s);
 
+// Frame synthesizer (synth.cu).
+struct SynthParams {
+  int n_frames, n_ant, M, cp, n_data, qb, levels;
+  float qscale;
+  int pn_len;
+  long long tx_len;            // (1 + D) * (M + cp) samples after the preamble
+  long long n_samples;         // samples per rx row (>= offset + pn_len + tx_len)
+  long long offset;            // timing offset: noise-only samples in front
+  const float2* pilot;         // [M] subcarrier (shifted) order
+  const float* chips;          // [pn_len] bipolar PN
+  const uint8_t* bits;         // [F, D*M*qb]
+  const float2* resp;          // [F or 1, N, n_taps] channel response
+  int n_taps, resp_per_frame;
+  int noisy;
+  float snr_db;
+  unsigned long long seed;
+  float2* tx;                  // [F, tx_len] scratch
+  double* sig_part;            // [F*N, parts] scratch
+  float2* rx;                  // [F, N, n_samples]
+};
+cudaError_t launch_synth_bits(uint8_t* bits, long long n_per_frame, int n_frames, uint64_t seed, cudaStream_t s);
+cudaError_t launch_synth_gains(float2* resp, int rows, uint64_t seed, cudaStream_t s);
+cudaError_t launch_synth(const SynthParams& p, cudaStream_t s);
+size_t synth_sig_parts(long long pn_len, long long tx_len);
+
 }  // namespace ofdmrx

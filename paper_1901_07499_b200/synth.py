@@ -89,3 +89,87 @@ def synth_batch(cfg: OfdmConfig, n_data, seeds, snr_db=10.0, mode="flat_rayleigh
     L = (1 + n_data) * cfg.symbol_len
     rx = np.stack([c.streams[:, off: off + L] if strip_preamble else c.streams for c in caps])
     return rx.astype(np.complex64), np.stack([c.tx_bits for c in caps]), (0 if strip_preamble else caps[0].symbol0_offset)
+
+
+# ---------------------------------------------------------------------------
+# Device synthesizer: build_frame + apply_channel as
+# sm_100a kernels (csrc/synth.cu) behind ofdmrx_synth_frames.
+# ---------------------------------------------------------------------------
+
+CHANNEL_MODES = ("identity", "fixed_gains", "flat_rayleigh", "multipath")  # channel.py:13
+
+
+@dataclass
+class DeviceFrames:
+    """A synthesised batch on the GPU."""
+
+    rx: "object"             # torch complex64 [F, N, S]
+    bits: "object"           # torch uint8 [F, D*M*b] payload (PipelineResult truth)
+    response: "object"       # torch complex64 [F or 1, N, T] channel response used
+    symbol0_offset: int      # timing_offset + PN length
+    frame_start: int         # timing_offset
+
+
+def synth_frames(cfg: OfdmConfig, n_data, n_frames, *, seed=0, snr_db=10.0, mode="flat_rayleigh",
+                 timing_offset=0, bits=None, gains=None, taps=None, pilot=None, pn=None, n_samples=None,
+                 stream=None):
+    """Synthesize F captures on the current CUDA device.
+
+    Mirrors waveform.build_frame (payload bits exactly filling ``n_data``
+    symbols) + channel.apply_channel with ChannelModel(mode, gains, taps,
+    snr_db, timing_offset): ``gains`` [N] for fixed_gains, ``taps`` [N, T]
+    for multipath, flat_rayleigh draws CN(0,1) per (frame, antenna).
+    ``bits`` (uint8 [F, D*M*b], numpy or torch) default to device-drawn fair
+    bits.  snr_db=None is noiseless.  Returns DeviceFrames."""
+    import ctypes
+
+    import torch
+
+    from . import _lib, device
+    from .errors import ConfigurationError, ContractError
+
+    if mode not in CHANNEL_MODES:
+        raise ConfigurationError(f"channel mode must be one of {CHANNEL_MODES}")
+    if timing_offset < 0:
+        raise ConfigurationError("timing_offset must be >= 0")
+    dev = device.require_cuda()
+    f, n, m = int(n_frames), cfg.n_antennas, cfg.fft_len
+    nb = n_data * m * cfg.bits_per_qam_symbol
+    st = device.stream_handle(stream)
+    if bits is None:
+        bits_t = torch.empty((f, nb), dtype=torch.uint8, device=dev)
+        _lib.call("ofdmrx_synth_bits", device.ptr(bits_t), f, nb, int(seed), st)
+    else:
+        bits_t = torch.as_tensor(np.asarray(bits.cpu() if isinstance(bits, torch.Tensor) else bits,
+                                            dtype=np.uint8)).reshape(f, nb).to(dev).contiguous()
+    if mode == "identity":
+        resp = torch.ones((1, n, 1), dtype=torch.complex64, device=dev)
+    elif mode == "fixed_gains":
+        if gains is None or len(gains) != n:
+            raise ConfigurationError("fixed_gains needs one gain per antenna")
+        resp = torch.from_numpy(np.asarray(gains, dtype=np.complex64).reshape(1, n, 1)).to(dev)
+    elif mode == "flat_rayleigh":
+        resp = torch.empty((f, n, 1), dtype=torch.complex64, device=dev)
+        _lib.call("ofdmrx_synth_rayleigh", device.ptr(resp), f * n, int(seed), st)
+    else:
+        t = np.asarray(taps, dtype=np.complex64)
+        if t.ndim != 2 or t.shape[0] != n:
+            raise ConfigurationError("multipath needs taps [n_antennas, T]")
+        resp = torch.from_numpy(np.ascontiguousarray(t)[None]).to(dev)
+    pv = pilot.values if pilot is not None and hasattr(pilot, "values") else pilot
+    pv = make_pilot(m).values if pv is None else np.asarray(pv)
+    if pv.shape != (m,):
+        raise ContractError(f"pilot has {pv.shape} values, config needs ({m},)")
+    chips = generate_pn_chips(length=cfg.pn_len) if pn is None else np.asarray(getattr(pn, "chips", pn), float)
+    pilot_t = torch.from_numpy(pv.astype(np.complex64)).to(dev)
+    chips_t = torch.from_numpy(chips.astype(np.float32)).to(dev)
+    frame_len = chips.size + (1 + n_data) * cfg.symbol_len
+    s = int(n_samples) if n_samples is not None else timing_offset + frame_len
+    rx = torch.empty((f, n, s), dtype=torch.complex64, device=dev)
+    desc = _lib.SynthDesc(f, n, m, cfg.cp_len, int(n_data), cfg.qam_order, int(chips.size), int(resp.shape[2]),
+                          int(resp.shape[0] > 1 or mode == "flat_rayleigh"), int(snr_db is not None),
+                          float(snr_db if snr_db is not None else 0.0), int(timing_offset), s, int(seed))
+    _lib.call("ofdmrx_synth_frames", ctypes.byref(desc), device.ptr(pilot_t), device.ptr(chips_t),
+              device.ptr(bits_t), device.ptr(resp), device.ptr(rx), st)
+    return DeviceFrames(rx=rx, bits=bits_t, response=resp, symbol0_offset=int(timing_offset + chips.size),
+                        frame_start=int(timing_offset))
