@@ -377,7 +377,10 @@ def run_b200(args, cfg_name, world, rank, local):
     if args.e2e_frames > 0:
         line["e2e"] = run_e2e(args, cfg, x, s0, d, world)
     if not args.no_stages and world == 1 and cfg_name != "C4":
-        line["stages"] = run_stages(args, cfg, x, s0, d)
+        try:
+            line["stages"] = run_stages(args, cfg, x, s0, d)
+        except Exception as exc:  # noqa: BLE001
+            line["stages"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_port_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds)
     return line
@@ -481,8 +484,16 @@ def run_stages(args, cfg, x_dev, s0, d, with_sync=True):
     out = frames.allocate_outputs(Fs, n, m, d, cfg.qam_order, x.device)
     t_fused, _ = timed(lambda: frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out))
     del Y, Yp, Yd, H
-    sync = run_sync_stage(cfg, d, Fs, timed) if with_sync else None
-    synth_t = run_synth_stage(cfg, d, Fs, timed) if with_sync else None
+    sync = synth_t = None
+    if with_sync:  # auxiliary §8(f) stages must never cost the bench line
+        try:
+            sync = run_sync_stage(cfg, d, Fs, timed)
+        except Exception as exc:  # noqa: BLE001
+            sync = {"error": repr(exc)[:300]}
+        try:
+            synth_t = run_synth_stage(cfg, d, Fs, timed)
+        except Exception as exc:  # noqa: BLE001
+            synth_t = {"error": repr(exc)[:300]}
     res = {"frames": Fs,
            "fft_us_per_symbol": t_fft / (Fs * (1 + d)),
            "ls_us_per_pilot_symbol": t_ls / Fs,

@@ -161,8 +161,11 @@ def synth_frames(cfg: OfdmConfig, n_data, n_frames, *, seed=0, snr_db=10.0, mode
     if pv.shape != (m,):
         raise ContractError(f"pilot has {pv.shape} values, config needs ({m},)")
     chips = generate_pn_chips(length=cfg.pn_len) if pn is None else np.asarray(getattr(pn, "chips", pn), float)
-    pilot_t = torch.from_numpy(pv.astype(np.complex64)).to(dev)
-    chips_t = torch.from_numpy(chips.astype(np.float32)).to(dev)
+    from .frames import _PILOTS
+    from .sync import _CHIPS
+
+    pilot_t = _PILOTS.get(pv, dev)   # cached device copies: no H2D inside a graph capture
+    chips_t = _CHIPS.get(chips, dev)
     frame_len = chips.size + (1 + n_data) * cfg.symbol_len
     s = int(n_samples) if n_samples is not None else timing_offset + frame_len
     rx = torch.empty((f, n, s), dtype=torch.complex64, device=dev)
