@@ -262,7 +262,8 @@ extern "C" {
 int64_t ofdmrx_detect_scratch_bytes(int32_t n_frames, int32_t n_antennas, int64_t n_samples, int32_t n_chips) {
   if (n_frames < 0 || n_antennas < 1 || n_chips < 1 || n_samples < n_chips) return -1;
   const long long rows = (long long)n_frames * n_antennas;
-  return rows * 8 + rows * (n_samples - n_chips + 1) * 4;
+  // keys [rows] u64 | metrics [rows, wins] f32 | (pad to 16) chip spectrum [1024] cf32
+  return ((rows * 8 + rows * (n_samples - n_chips + 1) * 4 + 15) & ~15LL) + (long long)ofdmrx::sync_fft_scratch_bytes();
 }
 
 int ofdmrx_corr_metrics(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_samples, int64_t row_stride,
@@ -273,6 +274,8 @@ int ofdmrx_corr_metrics(const void* rx, int32_t n_frames, int32_t n_antennas, in
   if (n_frames == 0) return OFDMRX_OK;
   if (int rc = check_ptr(metrics, "metrics")) return rc;
   p.metrics = metrics;
+  // the metric array itself is the product here: the direct fp32 form
+  // (error <= 3 P 2^-24) rather than the FFT form detect screens with
   cudaError_t e = ofdmrx::launch_corr(p, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "corr_kernel launch");
   return OFDMRX_OK;
@@ -293,9 +296,16 @@ int ofdmrx_detect(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t 
   p.keys = static_cast<unsigned long long*>(scratch);
   p.metrics = reinterpret_cast<float*>(static_cast<char*>(scratch) + rows * 8);
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = ofdmrx::launch_corr(p, s);
-  if (e != cudaSuccess) return cuda_fail(e, "corr_kernel launch");
-  e = ofdmrx::launch_refine(p, peak_index, peak_metric, s);
+  const bool fft = ofdmrx::sync_use_fft(n_chips);
+  cudaError_t e;
+  if (fft) {
+    const long long off = (rows * 8 + rows * p.wins * 4 + 15) & ~15LL;
+    e = ofdmrx::launch_corr_fft(p, reinterpret_cast<float2*>(static_cast<char*>(scratch) + off), 1, s);
+  } else {
+    e = ofdmrx::launch_corr(p, s);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "corr kernel launch");
+  e = ofdmrx::launch_refine(p, peak_index, peak_metric, fft ? 1 : 0, s);
   if (e != cudaSuccess) return cuda_fail(e, "refine_kernel launch");
   return OFDMRX_OK;
 }

@@ -100,7 +100,13 @@ struct SyncParams {
 };
 size_t sync_smem_bytes(int n_chips);
 cudaError_t launch_corr(const SyncParams& p, cudaStream_t s);
-cudaError_t launch_refine(const SyncParams& p, int32_t* peak_idx, double* peak_metric, cudaStream_t s);
+cudaError_t launch_refine(const SyncParams& p, int32_t* peak_idx, double* peak_metric, int bound_mode,
+                          cudaStream_t s);
+// overlap-save FFT correlation for 64 <= n_chips <= 960 (cspec: 1024 cf32 scratch);
+// bound_mode 1 writes per-window upper bounds and keys on lower bounds (detect)
+bool sync_use_fft(int n_chips);
+size_t sync_fft_scratch_bytes();
+cudaError_t launch_corr_fft(const SyncParams& p, float2* cspec, int bound_mode, cudaStream_t s);
 
 // Frame synthesizer (synth.cu).
 struct SynthParams {
