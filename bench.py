@@ -636,8 +636,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default per config)")
-    ap.add_argument("--e2e-frames", type=int, default=128)
-    ap.add_argument("--e2e-chunk", type=int, default=16)
+    ap.add_argument("--e2e-frames", type=int, default=256)
+    ap.add_argument("--e2e-chunk", type=int, default=32)
     ap.add_argument("--stage-frames", type=int, default=64)
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

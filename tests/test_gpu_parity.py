@@ -368,3 +368,29 @@ def test_stage_symbols_drops_cp_and_matches_full_receive(P, layout):
     assert torch.equal(got.bits, full.bits)
     assert torch.equal(got.s_hat, full.s_hat)
     assert torch.equal(got.H, full.H)
+
+
+@pytest.mark.parametrize("n_ant,m,cp,qam,d,nf", [(8, 64, 16, 16, 6, 3), (64, 1024, 72, 16, 10, 2), (16, 256, 32, 64, 4, 2)])
+def test_fused_complex_unit_pilot(P, n_ant, m, cp, qam, d, nf):
+    """Any unit-modulus pilot (not only make_pilot's BPSK): the fused kernel's
+    general H = Y conj(P) path (ls_divide, receiver.py:95-96), including the
+    on-device antenna-shard path at 64 antennas x 2 frames."""
+    rng = np.random.default_rng(m + n_ant)
+    pilot = np.exp(2j * np.pi * rng.random(m))
+    caps = []
+    for f in range(nf):
+        bits = np.random.default_rng(100 + f).integers(0, 2, size=d * m * int(math.log2(qam)), dtype=np.uint8)
+        tx, _, _ = orc.build_frame_samples(m, cp, qam, pilot, bits, orc.generate_pn())
+        st, _ = orc.apply_channel(tx, n_ant, mode="flat_rayleigh", snr_db=12.0, rng_seed=f)
+        caps.append(st)
+    streams = np.stack(caps)
+    cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    out = P.receive_frames(torch.from_numpy(streams.astype(np.complex64)).cuda(), cfg, pilot,
+                           symbol0_offset=255, n_data=d)
+    torch.cuda.synchronize()
+    for f in range(nf):
+        H, s_hat, w, bits = orc.receive_frame(streams[f], 255, m, cp, d, qam, pilot=pilot)
+        assert np.array_equal(out.bits[f].cpu().numpy(), bits)
+        assert rel(out.H[f].cpu().numpy(), H) < REL_TOL
+        assert rel(out.s_hat[f].cpu().numpy(), s_hat) < REL_TOL
+        assert rel(out.weights[f].cpu().numpy(), w) < REL_TOL
