@@ -288,7 +288,10 @@ def run_b200(args, cfg_name, world, rank, local):
     if args.frames:
         F = args.frames
     dev = torch.device("cuda", torch.cuda.current_device())
-    cfg, rx_host, bits_truth, s0 = make_inputs(cfg_name, seed_base=1000 * rank)
+    antenna_sharded = cfg_name == "C4" and world > 1
+    # frame sharding: distinct frames per rank; antenna sharding: every rank
+    # holds its antenna rows of the SAME frames
+    cfg, rx_host, bits_truth, s0 = make_inputs(cfg_name, seed_base=0 if antenna_sharded else 1000 * rank)
     base = torch.from_numpy(rx_host).to(dev)
     reps = (F + DISTINCT - 1) // DISTINCT
     x = base.repeat(reps, 1, 1)[:F].contiguous()
@@ -297,25 +300,32 @@ def run_b200(args, cfg_name, world, rank, local):
     stream = torch.cuda.current_stream()
 
     sharded = None
-    if cfg_name == "C4" and world > 1:
+    if antenna_sharded:
         # antenna-sharded MRC: every rank holds N/world antennas of the same frames
         from paper_1901_07499_b200 import sharding
 
         sharded = sharding.AntennaShardedReceiver(cfg, d, symbol0_offset=s0, mode=args.exchange)
         x = x[:, sharded.ant_lo:sharded.ant_hi].contiguous()
 
+    own = slice(None)
+    if sharded is not None and args.exchange == "peer":  # each rank finishes its F/world frames
+        own = slice(rank * (F // world), (rank + 1) * (F // world))
+
     def step():
         if sharded is not None:
             s_hat, w, bits, fl, _ = sharded.receive(x)
-            out.bits.copy_(bits)
-            out.flags.copy_(fl)
+            out.bits[own].copy_(bits)
+            out.flags[own].copy_(fl)
         else:
             frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out)
 
     # correctness spot-check of the benchmarked configuration (bits vs truth)
     step()
     torch.cuda.synchronize()
-    ber = float((out.bits[:DISTINCT].cpu().numpy() != bits_truth[: min(DISTINCT, F)]).mean())
+    lo = own.start or 0
+    hi = min(own.stop if own.stop is not None else F, lo + DISTINCT)
+    idx = np.arange(lo, hi)
+    ber = float((out.bits[lo:hi].cpu().numpy() != bits_truth[idx % len(bits_truth)]).mean())
     flags_bad = int((out.flags != 0).sum())
     for _ in range(max(0, args.warmup - 1)):
         step()
@@ -362,7 +372,8 @@ def run_b200(args, cfg_name, world, rank, local):
         "data": "synthetic: reference TX (PN|pilot|data, Gray QAM) through flat Rayleigh at 10 dB; "
                 f"{DISTINCT} distinct frames tiled on device",
         "config": {"workload": f"{cfg_name}: {n} ant x FFT {m} (CP {cp}), {qam}-QAM, 1 pilot + {d} data symbols/frame",
-                   "frames_per_gpu": F, "global_frames": F * world, "parallelism": (f"antenna-sharded x{world} ({args.exchange} exchange of MRC partials over NCCL)"
+                   "frames_per_gpu": F, "global_frames": F if sharded is not None else F * world, "parallelism": (f"antenna-sharded x{world} ({args.exchange} exchange of MRC partials"
+                                   f"{' over peer memory, no NCCL' if args.exchange == 'peer' else ' over NCCL'})"
                                    if sharded is not None else f"frame-sharded x{world}"),
                    "input_bytes_per_gpu": int(x.numel() * 8), "l2": "inputs 6.3 GB/GPU > L2, no flush needed"
                    if x.numel() * 8 > 126e6 else "inputs smaller than L2"},
@@ -642,7 +653,8 @@ def main():
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="gather", choices=["gather", "allreduce"])
+    ap.add_argument("--exchange", default="gather", choices=["gather", "allreduce", "peer"],
+                    help="C4 antenna-sharded exchange: NCCL all-gather / all-reduce, or fused peer-memory stores")
     ap.add_argument("--sweep", action="store_true", help="C5: antennas x FFT per-stage sweep -> CSV")
     ap.add_argument("--sweep-antennas", default="1,2,4,8,16,32,64,128")
     ap.add_argument("--sweep-ffts", default="64,128,256,512,1024,2048,4096")

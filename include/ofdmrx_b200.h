@@ -231,6 +231,34 @@ OFDMRX_API int ofdmrx_synth_rayleigh(void* resp, int32_t rows, uint64_t seed, vo
 OFDMRX_API int ofdmrx_synth_frames(const ofdmrx_synth_desc* desc, const void* pilot, const float* chips,
                                    const uint8_t* bits, const void* resp, void* rx, void* stream);
 
+/*
+ * Antenna-sharded exchange over peer memory, the fused
+ * alternative to gathering the partial sums with NCCL.  Each rank owns
+ * frames_per_owner consecutive frames and an inbox allocated with
+ * ofdmrx_peer_alloc (num [G, fpo, D, M] cf32 | den [G, fpo, M] f32 | flags),
+ * shared with the other ranks by CUDA IPC handle (64 bytes) and mapped with
+ * ofdmrx_peer_open (NVLink peer mapping across GPUs).
+ *
+ * ofdmrx_rx_partials_routed: ofdmrx_rx_partials whose epilogue stores frame
+ *   f's (num, den) straight into slot `slot` of owner f / fpo's inbox:
+ *   num_dst / den_dst are DEVICE arrays of G pointers (the owners' num / den
+ *   bases).  No NCCL call; the stores cross NVLink from the kernel.
+ * ofdmrx_peer_signal: st.release.sys of `value` to each of n device flag
+ *   addresses (device array dst_table), after the stream's previous work.
+ * ofdmrx_peer_wait: stream waits until each of n flags (ld.acquire.sys) is
+ *   >= value.
+ * The finish step is ofdmrx_mrc_finish over the own inbox.
+ */
+OFDMRX_API int ofdmrx_rx_partials_routed(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H,
+                                         const void* num_dst, const void* den_dst, int32_t frames_per_owner,
+                                         int32_t slot, uint32_t* flags, void* stream);
+OFDMRX_API int ofdmrx_peer_alloc(int64_t bytes, void** ptr, void* ipc_handle);
+OFDMRX_API int ofdmrx_peer_open(const void* ipc_handle, void** ptr);
+OFDMRX_API int ofdmrx_peer_close(void* ptr);
+OFDMRX_API int ofdmrx_peer_free(void* ptr);
+OFDMRX_API int ofdmrx_peer_signal(const void* dst_table, int32_t n, uint64_t value, void* stream);
+OFDMRX_API int ofdmrx_peer_wait(const void* src_table, int32_t n, uint64_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

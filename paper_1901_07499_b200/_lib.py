@@ -100,6 +100,13 @@ SIGNATURES = {
     "ofdmrx_synth_bits": (ctypes.c_int, [_p, _i32, _i64, ctypes.c_uint64, _p]),
     "ofdmrx_synth_rayleigh": (ctypes.c_int, [_p, _i32, ctypes.c_uint64, _p]),
     "ofdmrx_synth_frames": (ctypes.c_int, [_SDESC, _p, _p, _p, _p, _p, _p]),
+    "ofdmrx_rx_partials_routed": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _i32, _i32, _p, _p]),
+    "ofdmrx_peer_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(ctypes.c_void_p), _p]),
+    "ofdmrx_peer_open": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "ofdmrx_peer_close": (ctypes.c_int, [_p]),
+    "ofdmrx_peer_free": (ctypes.c_int, [_p]),
+    "ofdmrx_peer_signal": (ctypes.c_int, [_p, _i32, ctypes.c_uint64, _p]),
+    "ofdmrx_peer_wait": (ctypes.c_int, [_p, _i32, ctypes.c_uint64, _p]),
 }
 
 _lock = threading.Lock()

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "../../include/ofdmrx_b200.h"
@@ -122,8 +123,15 @@ int scratch_alloc(void** ptr, size_t bytes, cudaStream_t st) {
   return OFDMRX_OK;
 }
 
+struct Route {  // partial sums routed to the owners' peer inboxes
+  const void* num_dst;
+  const void* den_dst;
+  int fpo, slot;
+};
+
 int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, int mode, void* H, void* s_hat,
-                 float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream) {
+                 float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream,
+                 const Route* route = nullptr) {
   if (int rc = check_desc_impl(d, -1)) return rc;
   if (d->n_frames == 0) return OFDMRX_OK;
   if (int rc = check_ptr(rx, "rx")) return rc;
@@ -134,10 +142,17 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
     if (int rc = check_ptr(bits, "bits")) return rc;
     if (int rc = check_align(bits, 4, "bits")) return rc;
   }
-  if (mode == 1) {
+  if (mode == 1 && route == nullptr) {
     if (d->n_data > 0)
       if (int rc = check_ptr(num, "num")) return rc;
     if (int rc = check_ptr(den, "den")) return rc;
+  }
+  if (route != nullptr) {
+    if (int rc = check_ptr(route->num_dst, "num_dst")) return rc;
+    if (int rc = check_ptr(route->den_dst, "den_dst")) return rc;
+    if (route->fpo < 1 || d->n_frames % route->fpo != 0)
+      return fail(OFDMRX_ERR_CONTRACT, "n_frames %d is not a multiple of frames_per_owner %d", d->n_frames, route->fpo);
+    if (route->slot < 0) return fail(OFDMRX_ERR_CONTRACT, "slot must be >= 0");
   }
   ofdmrx::FusedLaunch l{};
   cudaError_t e = ofdmrx::fused_plan(d->fft_len, d->n_frames, d->n_data, &l);
@@ -181,6 +196,12 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   p.flags = flags;
   p.part_num = static_cast<float2*>(num);
   p.part_den = den;
+  if (route != nullptr) {
+    p.num_dst = static_cast<float2* const*>(route->num_dst);
+    p.den_dst = static_cast<float* const*>(route->den_dst);
+    p.fpo = route->fpo;
+    p.slot = route->slot;
+  }
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (shards == 1) {
     e = ofdmrx::launch_fused(d->fft_len, p, l, st);
@@ -327,6 +348,64 @@ int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* 
 int ofdmrx_rx_partials(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* num,
                        float* den, uint32_t* flags, void* stream) {
   return fused_common(desc, rx, pilot, 1, H, nullptr, nullptr, nullptr, nullptr, flags, num, den, stream);
+}
+
+int ofdmrx_rx_partials_routed(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H,
+                              const void* num_dst, const void* den_dst, int32_t frames_per_owner, int32_t slot,
+                              uint32_t* flags, void* stream) {
+  const Route r{num_dst, den_dst, frames_per_owner, slot};
+  return fused_common(desc, rx, pilot, 1, H, nullptr, nullptr, nullptr, nullptr, flags, nullptr, nullptr, stream, &r);
+}
+
+int ofdmrx_peer_alloc(int64_t bytes, void** ptr, void* ipc_handle) {
+  if (bytes <= 0) return fail(OFDMRX_ERR_CONTRACT, "bytes must be > 0");
+  if (int rc = check_ptr(ptr, "ptr")) return rc;
+  if (int rc = check_ptr(ipc_handle, "ipc_handle")) return rc;
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc (peer inbox)");
+  if ((e = cudaMemset(*ptr, 0, (size_t)bytes)) != cudaSuccess) return cuda_fail(e, "cudaMemset (peer inbox)");
+  cudaIpcMemHandle_t h;
+  if ((e = cudaIpcGetMemHandle(&h, *ptr)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  memcpy(ipc_handle, &h, sizeof(h));
+  return OFDMRX_OK;
+}
+
+int ofdmrx_peer_open(const void* ipc_handle, void** ptr) {
+  if (int rc = check_ptr(ipc_handle, "ipc_handle")) return rc;
+  if (int rc = check_ptr(ptr, "ptr")) return rc;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return OFDMRX_OK;
+}
+
+int ofdmrx_peer_close(void* ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? OFDMRX_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+int ofdmrx_peer_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? OFDMRX_OK : cuda_fail(e, "cudaFree (peer inbox)");
+}
+
+int ofdmrx_peer_signal(const void* dst_table, int32_t n, uint64_t value, void* stream) {
+  if (n < 0) return fail(OFDMRX_ERR_CONTRACT, "n must be >= 0");
+  if (n > 0)
+    if (int rc = check_ptr(dst_table, "dst_table")) return rc;
+  cudaError_t e = ofdmrx::launch_peer_signal(static_cast<unsigned long long* const*>(dst_table), n,
+                                             (unsigned long long)value, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? OFDMRX_OK : cuda_fail(e, "peer_signal_kernel launch");
+}
+
+int ofdmrx_peer_wait(const void* src_table, int32_t n, uint64_t value, void* stream) {
+  if (n < 0) return fail(OFDMRX_ERR_CONTRACT, "n must be >= 0");
+  if (n > 0)
+    if (int rc = check_ptr(src_table, "src_table")) return rc;
+  cudaError_t e = ofdmrx::launch_peer_wait(static_cast<const unsigned long long* const*>(src_table), n,
+                                           (unsigned long long)value, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? OFDMRX_OK : cuda_fail(e, "peer_wait_kernel launch");
 }
 
 int ofdmrx_mrc_finish(int32_t n_frames, int32_t n_data, int32_t fft_len, int32_t qam_order, int32_t n_parts,

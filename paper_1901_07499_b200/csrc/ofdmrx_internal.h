@@ -34,6 +34,12 @@ struct FusedParams {
   uint32_t* flags;         // [F]
   float2* part_num;        // [S, F, D, M]         (mode 1, required)
   float* part_den;         // [S, F, M]            (mode 1, required)
+  // mode 1 routed to peers (antenna-sharded exchange over peer memory):
+  // frame f goes to owner o = f / fpo, slot `slot` of its inbox
+  // num_dst[o] [G, fpo, D, M] and den_dst[o] [G, fpo, M]
+  float2* const* num_dst;
+  float* const* den_dst;
+  int fpo, slot;
 };
 
 struct FusedLaunch {
@@ -132,5 +138,9 @@ cudaError_t launch_synth_bits(uint8_t* bits, long long n_per_frame, int n_frames
 cudaError_t launch_synth_gains(float2* resp, int rows, uint64_t seed, cudaStream_t s);
 cudaError_t launch_synth(const SynthParams& p, cudaStream_t s);
 size_t synth_sig_parts(long long pn_len, long long tx_len);
+
+// Peer-memory exchange flags (peer.cu)
+cudaError_t launch_peer_signal(unsigned long long* const* dst, int n, unsigned long long value, cudaStream_t s);
+cudaError_t launch_peer_wait(const unsigned long long* const* src, int n, unsigned long long value, cudaStream_t s);
 
 }  // namespace ofdmrx

@@ -321,8 +321,14 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     }
     if (active && chunk == 0) {
       float* wdst = p.mode == 0 ? p.weights : p.part_den;
+      long long wrow = (long long)shard * p.n_frames + f;
+      if (p.mode == 1 && p.den_dst != nullptr) {  // routed to the frame's owner
+        const int o = f / p.fpo;
+        wdst = p.den_dst[o];
+        wrow = (long long)p.slot * p.fpo + (f - o * p.fpo);
+      }
       if (wdst != nullptr) {
-        float* w = wdst + ((long long)shard * p.n_frames + f) * M + t;
+        float* w = wdst + wrow * M + t;
 #pragma unroll
         for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = den[i];
       }
@@ -346,6 +352,10 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
       }
     } else {
       float2* ndst = p.part_num + sym_base + t;
+      if (p.num_dst != nullptr) {
+        const int o = f / p.fpo;
+        ndst = p.num_dst[o] + (((long long)p.slot * p.fpo + (f - o * p.fpo)) * p.n_data + d) * M + t;
+      }
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         if (!isfinite(a[2 * i]) || !isfinite(a[2 * i + 1])) flag |= 1u;
@@ -354,6 +364,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     }
   }
   if (flag != 0u && p.flags != nullptr) atomicOr(&p.flags[f], flag);
+  if (p.num_dst != nullptr) __threadfence_system();  // peer stores before the exchange flags
 }
 
 template <int M>

@@ -15,8 +15,15 @@
       (numerics.py:85-106) when the shard size is a power of two;
     - "allreduce": one NCCL sum all-reduce of the packed partials (half the
       bytes on the wire, association order left to NCCL).
-  The exchange functions only use torch.distributed collectives, so they run
-  unchanged on the gloo backend for the CPU tests.
+    - "peer": no collective on the data path.  Each rank owns F/G frames; the
+      fused partial-sum kernel stores every frame's (num, den) straight into
+      the owner's inbox over peer memory (CUDA IPC mappings: NVLink stores
+      between GPUs), release/acquire flags hand the inbox to its owner, which
+      runs the same pairwise-tree finish over the G slots (PeerExchange).
+      Each rank returns its own F/G frames (reduce-scatter semantics).
+  "gather"/"allreduce" only use torch.distributed collectives, so they run
+  unchanged on the gloo backend for the CPU tests; "peer" uses
+  torch.distributed only once, to exchange the 64-byte IPC handles.
 """
 
 import numpy as np
@@ -25,7 +32,7 @@ import torch.distributed as dist
 
 from .errors import ConfigurationError, ContractError
 
-EXCHANGE_MODES = ("gather", "allreduce")
+EXCHANGE_MODES = ("gather", "allreduce", "peer")
 
 
 def frame_shard(n_frames, rank, world):
@@ -97,6 +104,83 @@ def tree_sum_parts(x):
     return acc[0]
 
 
+class PeerExchange:
+    """Inboxes and flags of the peer-memory exchange for one rank.
+
+    Inbox of rank r (one ofdmrx_peer_alloc allocation, zero-initialised):
+      num [G, fpo, D, M] cf32 | den [G, fpo, M] f32 | ready [G] u64 | consumed u64
+    slot g of num/den holds producer g's partial sums of r's frames; ready[g]
+    is producer g's epoch flag; consumed is r's "inbox read" epoch."""
+
+    def __init__(self, n_frames, n_data, fft_len, group=None, device=None):
+        import ctypes
+
+        from . import _lib
+        from . import device as dv
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if n_frames % self.world:
+            raise ConfigurationError(f"{n_frames} frames do not split evenly over {self.world} owners")
+        self.fpo = n_frames // self.world
+        self.n_frames, self.n_data, self.fft_len = n_frames, n_data, fft_len
+        g, fpo, d, m = self.world, self.fpo, n_data, fft_len
+        self.num_bytes = g * fpo * d * m * 8
+        self.den_off = self.num_bytes
+        self.ready_off = (self.den_off + g * fpo * m * 4 + 15) // 16 * 16
+        self.consumed_off = self.ready_off + 8 * g
+        nbytes = self.consumed_off + 64
+        self.dev = dv.require_cuda(device)
+        lib = _lib.load()
+        ptr = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(lib.ofdmrx_peer_alloc(nbytes, ctypes.byref(ptr), handle))
+        self.own = ptr.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self.bases, self.opened = [], []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.bases.append(self.own)
+                continue
+            q = ctypes.c_void_p()
+            _lib.check(lib.ofdmrx_peer_open(ctypes.create_string_buffer(h, 64), ctypes.byref(q)))
+            self.bases.append(q.value)
+            self.opened.append(q.value)
+        b = self.bases
+        tab = lambda xs: torch.tensor(xs, dtype=torch.int64, device=self.dev)  # noqa: E731
+        self.num_dst = tab(b)
+        self.den_dst = tab([x + self.den_off for x in b])
+        self.ready_dst = tab([x + self.ready_off + 8 * self.rank for x in b])  # my flag at every owner
+        self.ready_src = tab([self.own + self.ready_off + 8 * i for i in range(g)])  # producers' flags here
+        self.consumed_src = tab([x + self.consumed_off for x in b])
+        self.consumed_dst = tab([self.own + self.consumed_off])
+        self.epoch = 0
+        self.group = group
+
+    def inbox(self):
+        """(num [G, fpo, D, M], den [G, fpo, M]) views of this rank's inbox as
+        raw pointers for ofdmrx_mrc_finish."""
+        return self.own, self.own + self.den_off
+
+    def close(self):
+        from . import _lib
+
+        lib = _lib.load()
+        for q in self.opened:
+            lib.ofdmrx_peer_close(ctypes_void(q))
+        self.opened = []
+        if self.own:
+            lib.ofdmrx_peer_free(ctypes_void(self.own))
+            self.own = None
+
+
+def ctypes_void(v):
+    import ctypes
+
+    return ctypes.c_void_p(int(v))
+
+
 class AntennaShardedReceiver:
     """Antenna-sharded fused receive for one rank of a process group.
 
@@ -119,16 +203,71 @@ class AntennaShardedReceiver:
         self.ant_lo, self.ant_hi = antenna_shard(cfg.n_antennas, self.rank, self.world)
         self.shard_cfg = OfdmConfig(cfg.fft_len, cfg.cp_len, self.ant_hi - self.ant_lo, qam_order=cfg.qam_order,
                                     pn_len=cfg.pn_len)
+        self.peer = None
 
     def receive(self, rx_shard, want_h=False, stream=None):
         from . import frames
 
+        if self.mode == "peer":
+            return self._receive_peer(rx_shard, want_h, stream)
         H, num, den, flags = frames.receive_partials(rx_shard, self.shard_cfg, self.pilot,
                                                      symbol0_offset=self.symbol0_offset, n_data=self.n_data,
                                                      want_h=want_h, stream=stream)
         nump, denp = exchange_partials(num, den, self.mode, self.group)
         s_hat, weights, bits, fflags = frames.finish_partials(nump, denp, self.cfg.qam_order, stream=stream)
         return s_hat, weights, bits, fflags | flags, H
+
+    def _receive_peer(self, rx_shard, want_h, stream):
+        """Fused partials -> owners' inboxes (peer stores) -> flags -> finish of
+        the own frames.  Returns (s_hat, weights, bits, flags, H) for frames
+        [rank * F/G, (rank + 1) * F/G)."""
+        import ctypes
+
+        from . import _lib, device as dv, frames
+
+        x = dv.as_c64(rx_shard, dv.require_cuda(rx_shard.device if isinstance(rx_shard, torch.Tensor) else None))
+        if x.dim() == 2:
+            x = x[None]
+        f, n, s = x.shape
+        ex = self.peer
+        if ex is None or ex.n_frames != f:
+            if ex is not None:
+                ex.close()
+            ex = self.peer = PeerExchange(f, self.n_data, self.cfg.fft_len, self.group, x.device)
+        ex.epoch += 1
+        e = ex.epoch
+        st = dv.stream_handle(stream)
+        g, m, d = ex.world, self.cfg.fft_len, self.n_data
+        lib = _lib.load()
+        # owners have read epoch e-1 from their inboxes
+        _lib.check(lib.ofdmrx_peer_wait(dv.ptr(ex.consumed_src), g, e - 1, st))
+        pvals = frames._pilot_values(self.pilot, m)
+        desc = dv.make_desc(f, n, m, self.cfg.cp_len, d, self.cfg.qam_order, self.symbol0_offset, s, n * s,
+                            options=dv.pilot_options(pvals))
+        H = torch.empty((f, n, m), dtype=torch.complex64, device=x.device) if want_h else None
+        flags = torch.zeros((f,), dtype=torch.int32, device=x.device)
+        pv = frames._PILOTS.get(pvals, x.device)
+        _lib.call("ofdmrx_rx_partials_routed", ctypes.byref(desc), dv.ptr(x), dv.ptr(pv), dv.ptr(H),
+                  dv.ptr(ex.num_dst), dv.ptr(ex.den_dst), ex.fpo, ex.rank, dv.ptr(flags), st)
+        _lib.check(lib.ofdmrx_peer_signal(dv.ptr(ex.ready_dst), g, e, st))
+        _lib.check(lib.ofdmrx_peer_wait(dv.ptr(ex.ready_src), g, e, st))
+        qb = dv.qam_bits(self.cfg.qam_order)
+        fo = ex.fpo
+        s_hat = torch.empty((fo, d, m), dtype=torch.complex64, device=x.device)
+        weights = torch.empty((fo, m), dtype=torch.float32, device=x.device)
+        bits = torch.empty((fo, d * m * qb), dtype=torch.uint8, device=x.device)
+        fflags = torch.zeros((fo,), dtype=torch.int32, device=x.device)
+        num_p, den_p = ex.inbox()
+        _lib.call("ofdmrx_mrc_finish", fo, d, m, int(self.cfg.qam_order), g, ctypes_void(num_p), ctypes_void(den_p),
+                  float(dv.MRC_WEIGHT_FLOOR), dv.ptr(s_hat), dv.ptr(weights), dv.ptr(bits), dv.ptr(fflags), st)
+        _lib.check(lib.ofdmrx_peer_signal(dv.ptr(ex.consumed_dst), 1, e, st))
+        own = slice(ex.rank * fo, (ex.rank + 1) * fo)
+        return s_hat, weights, bits, fflags | flags[own], (H[own] if H is not None else None)
+
+    def close(self):
+        if getattr(self, "peer", None) is not None:
+            self.peer.close()
+            self.peer = None
 
     def exchange_bytes(self, n_frames):
         """Bytes each rank contributes to the exchange per call."""
