@@ -182,6 +182,60 @@ def cpu_port_baseline(cfg_name, rx_host, budget_s=10.0):
                       f"receive_frame (numpy radix-2 as reference numpy_backend), {dt:.1f} s"}
 
 
+_REF_NUMPY_SNIPPET = r"""
+import json, sys, time
+import numpy as np
+from ofdmrx import receiver as rref, waveform as wref
+from ofdmrx.kernels import BACKEND
+from ofdmrx.sync import DetectionResult
+x = np.load(sys.argv[1]).astype(np.complex128)
+m, cp, n, qam, d, budget = (float(v) if i == 5 else int(v) for i, v in enumerate(sys.argv[2:8]))
+cfg = wref.OfdmConfig(m, cp, n, qam_order=qam)
+pilot = wref.make_pilot(m)
+class Cap:
+    def __init__(self, s): self.streams = s
+det = DetectionResult(True, 0, 0, 1.0, ())
+slots = [rref.extract_slots(Cap(f), det, cfg, 1 + d) for f in x]
+eng = rref.make_engine(rref.EngineKind("sequential"))
+frames, t0 = 0, time.perf_counter()
+while time.perf_counter() - t0 < budget:
+    rref.run_ring_pipeline(slots[frames % len(slots)], cfg, eng, pilot=pilot)
+    frames += 1
+dt = time.perf_counter() - t0
+print(json.dumps({"frames": frames, "seconds": dt, "backend": BACKEND}))
+"""
+
+
+def cpu_reference_numpy_baseline(cfg_name, rx_host, budget_s=10.0):
+    """The reference's own numpy CPU path (baseline/_ref with
+    OFDMRX_BACKEND=numpy: the north star's "reference numpy CPU path"),
+    SequentialEngine, 1 thread, timed in a subprocess (the backend is fixed
+    at import) on a bounded sample of the same frames.  None if the
+    reference is not installed."""
+    import tempfile
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "ofdmrx")):
+        return None
+    n, m, cp, qam, d, _ = CONFIGS[cfg_name]
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "frames.npy")
+        np.save(path, rx_host)
+        env = dict(os.environ, OFDMRX_BACKEND="numpy", PYTHONPATH=ref, OMP_NUM_THREADS="1",
+                   OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+        try:
+            out = subprocess.run([sys.executable, "-c", _REF_NUMPY_SNIPPET, path, str(m), str(cp), str(n), str(qam),
+                                  str(d), str(budget_s)], env=env, capture_output=True, text=True,
+                                 timeout=budget_s * 4 + 120)
+            res = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception:  # noqa: BLE001
+            return None
+    return {"value": res["frames"] * (1 + d) / res["seconds"], "unit": "symbols/s", "cores": 1, "kind": "reference",
+            "sample": f"{res['frames']} {cfg_name} frames ({res['frames'] * (1 + d)} OFDM symbols), unmodified "
+                      f"reference ofdmrx run_ring_pipeline, backend={res['backend']}, SequentialEngine, "
+                      f"{res['seconds']:.1f} s"}
+
+
 def reference_importable():
     ref = os.path.join(ROOT, "baseline", "_ref")
     if os.path.isdir(os.path.join(ref, "ofdmrx")):
@@ -393,7 +447,8 @@ def run_b200(args, cfg_name, world, rank, local):
         except Exception as exc:  # noqa: BLE001
             line["stages"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_port_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds)
+        line["cpu_baseline"] = (cpu_reference_numpy_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds)
+                                or cpu_port_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds))
     return line
 
 
