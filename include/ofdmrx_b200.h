@@ -80,6 +80,10 @@ typedef struct {
 /* desc.options: the caller asserts every pilot value is exactly +1 or -1
  * (make_pilot's BPSK pilot, waveform.py:214-220); H = Y/P becomes a sign flip. */
 #define OFDMRX_OPT_PILOT_BPSK 1
+/* desc.options: never split a frame's antennas into on-device shards (one
+ * CTA per frame even for small batches; results then do not depend on the
+ * batch size). */
+#define OFDMRX_OPT_NO_SHARDS 2
 
 OFDMRX_API int ofdmrx_abi_version(void);
 OFDMRX_API const char* ofdmrx_last_error(void);

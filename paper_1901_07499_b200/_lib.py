@@ -25,6 +25,7 @@ OK, ERR_CONFIG, ERR_CONTRACT, ERR_INPUT, ERR_NUMERIC, ERR_CUDA = range(6)
 FLAG_NONFINITE = 1
 FLAG_ERASED = 2
 OPT_PILOT_BPSK = 1
+OPT_NO_SHARDS = 2
 
 _STATUS_EXC = {
     ERR_CONFIG: ConfigurationError,

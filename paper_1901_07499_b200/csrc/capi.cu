@@ -58,7 +58,8 @@ int check_qam(int order) {
 
 int check_desc_impl(const ofdmrx_frame_desc* d, long long rx_len) {
   if (d == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
-  if ((d->options & ~OFDMRX_OPT_PILOT_BPSK) != 0) return fail(OFDMRX_ERR_CONTRACT, "unknown descriptor options 0x%x", d->options);
+  if ((d->options & ~(OFDMRX_OPT_PILOT_BPSK | OFDMRX_OPT_NO_SHARDS)) != 0)
+    return fail(OFDMRX_ERR_CONTRACT, "unknown descriptor options 0x%x", d->options);
   if (int rc = check_fft_len(d->fft_len)) return rc;
   if (d->cp_len < 0 || d->cp_len >= d->fft_len)
     return fail(OFDMRX_ERR_CONFIG, "cp_len must satisfy 0 <= cp_len < fft_len, got %d", d->cp_len);
@@ -101,7 +102,7 @@ int check_align(const void* p, unsigned a, const char* what) {
 int pick_shards(const ofdmrx_frame_desc* d, const ofdmrx::FusedLaunch& l) {
   const long long ctas = ((long long)d->n_frames * l.n_chunks + l.fpb - 1) / l.fpb;
   int s = 1;
-  if (d->n_data == 0) return 1;  // pilot-only frames: nothing to combine
+  if (d->n_data == 0 || (d->options & OFDMRX_OPT_NO_SHARDS)) return 1;  // pilot-only frames: nothing to combine
   while (ctas * s < 3 * 148 && d->n_antennas % (2 * s) == 0 && d->n_antennas / (2 * s) >= 16 && s < 64) s *= 2;
   return s;
 }
@@ -203,6 +204,18 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
     p.slot = route->slot;
   }
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (route == nullptr && ofdmrx::balanced_eligible(d->fft_len, d->n_antennas, d->n_data, mode, zf != nullptr, shards)) {
+    void* hscratch = nullptr;
+    if (p.H == nullptr) {  // H travels through L2 between the phases: scratch when the caller wants none
+      if (int rc = scratch_alloc(&hscratch, (size_t)d->n_frames * d->n_antennas * d->fft_len * 8, st)) return rc;
+      p.H = static_cast<float2*>(hscratch);
+    }
+    e = ofdmrx::launch_balanced(p, st);
+    cudaError_t e2 = hscratch != nullptr ? cudaFreeAsync(hscratch, st) : cudaSuccess;
+    if (e != cudaSuccess) return cuda_fail(e, "rx_balanced_kernel launch");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
+    return OFDMRX_OK;
+  }
   if (shards == 1) {
     e = ofdmrx::launch_fused(d->fft_len, p, l, st);
     if (e != cudaSuccess) return cuda_fail(e, "rx_fused_kernel launch");

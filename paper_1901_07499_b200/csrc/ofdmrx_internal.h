@@ -47,6 +47,12 @@ struct FusedLaunch {
   size_t smem;
 };
 
+// Balanced M = 1024 variant (rx_balanced.cu): pilot rows first, data rows split
+// evenly over the warps, H through L2.  Needs p.H (caller supplies scratch).
+bool balanced_eligible(int M, int n_ant, int n_data, int mode, bool zf, int shards);
+size_t balanced_smem_bytes();
+cudaError_t launch_balanced(const FusedParams& p, cudaStream_t s);
+
 // returns cudaErrorInvalidValue for unsupported M
 cudaError_t fused_plan(int M, int n_frames, int n_data, FusedLaunch* out);
 cudaError_t launch_fused(int M, const FusedParams& p, const FusedLaunch& l, cudaStream_t s);

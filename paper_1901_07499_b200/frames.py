@@ -90,7 +90,7 @@ def allocate_outputs(n_frames, n_antennas, fft_len, n_data, qam_order, dev, want
 
 
 def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
-                   out=None, want_h=True, zf=False, check=False, stream=None):
+                   out=None, want_h=True, zf=False, check=False, stream=None, shards=True):
     """Fused receive of a batch of captures on the current CUDA device.
 
     rx: complex64 CUDA tensor [F, N, S] or [N, S] (numpy is copied H2D).
@@ -113,13 +113,13 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     if n_data < 0 or symbol0_offset < 0:
         raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
     desc_args = (f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
-    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream)
+    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards)
 
 
-def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream):
+def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards=True):
     f, n, _, _, n_data = desc_args[:5]
     pvals = _pilot_values(pilot, cfg.fft_len)
-    desc = device.make_desc(*desc_args, options=device.pilot_options(pvals))
+    desc = device.make_desc(*desc_args, options=device.pilot_options(pvals) | (0 if shards else _lib.OPT_NO_SHARDS))
     device.check_desc(desc, x.numel())
     pv = _PILOTS.get(pvals, x.device)
     if out is None:

@@ -394,3 +394,35 @@ def test_fused_complex_unit_pilot(P, n_ant, m, cp, qam, d, nf):
         assert rel(out.H[f].cpu().numpy(), H) < REL_TOL
         assert rel(out.s_hat[f].cpu().numpy(), s_hat) < REL_TOL
         assert rel(out.weights[f].cpu().numpy(), w) < REL_TOL
+
+
+@pytest.mark.parametrize("n_ant,d,nf,bpsk", [(64, 10, 3, True), (8, 12, 2, True), (5, 3, 2, True), (100, 1, 2, True),
+                                             (13, 7, 2, False), (1, 12, 2, True), (64, 10, 2, False)])
+def test_balanced_kernel_m1024(P, n_ant, d, nf, bpsk):
+    """M = 1024 frames with one CTA per frame (no on-device shards): the
+    balanced kernel (rx_balanced.cu: pilot rows first, data rows split evenly
+    over the 12 warps, H through L2, symbols spanning warps combined in the
+    epilogue).  Covers ranges exactly N rows long, warps without rows, N < 12
+    and a single antenna."""
+    m, cp, qam = 1024, 72, 16
+    pilot = orc.make_pilot(m) if bpsk else np.exp(2j * np.pi * np.random.default_rng(n_ant).random(m))
+    caps = []
+    for f in range(nf):
+        bits = np.random.default_rng(200 + f).integers(0, 2, size=d * m * 4, dtype=np.uint8)
+        tx, _, _ = orc.build_frame_samples(m, cp, qam, pilot, bits, orc.generate_pn())
+        st, _ = orc.apply_channel(tx, n_ant, mode="flat_rayleigh", snr_db=15.0, rng_seed=f + 7)
+        caps.append(st)
+    streams = np.stack(caps)
+    cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    for want_h in (True, False):
+        out = P.receive_frames(torch.from_numpy(streams.astype(np.complex64)).cuda(), cfg, pilot,
+                               symbol0_offset=255, n_data=d, shards=False, want_h=want_h)
+        torch.cuda.synchronize()
+        assert int(out.flags.abs().sum()) == 0
+        for f in range(nf):
+            H, s_hat, w, bits = orc.receive_frame(streams[f], 255, m, cp, d, qam, pilot=pilot)
+            assert np.array_equal(out.bits[f].cpu().numpy(), bits)
+            assert rel(out.s_hat[f].cpu().numpy(), s_hat) < REL_TOL
+            assert rel(out.weights[f].cpu().numpy(), w) < REL_TOL
+            if want_h:
+                assert rel(out.H[f].cpu().numpy(), H) < REL_TOL
