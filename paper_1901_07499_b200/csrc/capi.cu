@@ -109,18 +109,27 @@ int pick_shards(const ofdmrx_frame_desc* d, const ofdmrx::FusedLaunch& l) {
 
 // stream-ordered scratch from the device's default pool, kept warm
 int scratch_alloc(void** ptr, size_t bytes, cudaStream_t st) {
-  static bool pool_set = false;
-  if (!pool_set) {
-    int dev = 0;
+  // a private pool per device (the process-wide default pool keeps its own
+  // release threshold); scratch stays mapped between calls
+  static cudaMemPool_t pools[32] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 32 && pools[dev] == nullptr) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
       uint64_t keep = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = pool;
     }
-    pool_set = true;
   }
-  cudaError_t e = cudaMallocAsync(ptr, bytes, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (shard partials)");
+  e = dev < 32 && pools[dev] != nullptr ? cudaMallocFromPoolAsync(ptr, bytes, pools[dev], st)
+                                        : cudaMallocAsync(ptr, bytes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (scratch)");
   return OFDMRX_OK;
 }
 

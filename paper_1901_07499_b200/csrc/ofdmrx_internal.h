@@ -6,6 +6,21 @@
 
 namespace ofdmrx {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device;
+// `done` is the call site's static bit set of devices already configured
+// (idempotent, so a race only repeats the attribute write).
+template <typename K>
+inline cudaError_t ensure_smem_attr(K kernel, int bytes, unsigned& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned bit = dev < 32 ? 1u << dev : 0u;
+  if (bit != 0u && (done & bit) != 0u) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done |= bit;
+  return e;
+}
+
 // Fused receive: one CTA processes FPB work items; a work item is one
 // (frame, chunk of data symbols) pair and owns 1 + DC "symbol lanes"
 // (lane 0 = pilot).  Every lane streams its symbol's antenna rows through

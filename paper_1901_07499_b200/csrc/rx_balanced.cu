@@ -326,15 +326,11 @@ size_t balanced_smem_bytes() { return BBAR + (size_t)BW * 2 * BSS * sizeof(float
 
 cudaError_t launch_balanced(const FusedParams& p, cudaStream_t s) {
   if (p.n_frames == 0) return cudaSuccess;
-  static bool attr_set = false;
+  static unsigned done_t = 0, done_f = 0;
   const size_t smem = balanced_smem_bytes();
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rx_balanced_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(rx_balanced_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = ensure_smem_attr(rx_balanced_kernel<true>, (int)smem, done_t);
+  if (e == cudaSuccess) e = ensure_smem_attr(rx_balanced_kernel<false>, (int)smem, done_f);
+  if (e != cudaSuccess) return e;
   if (p.pilot_bpsk) rx_balanced_kernel<true><<<p.n_frames, BW * 32, smem, s>>>(p);
   else rx_balanced_kernel<false><<<p.n_frames, BW * 32, smem, s>>>(p);
   return cudaGetLastError();

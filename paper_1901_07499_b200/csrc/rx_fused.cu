@@ -415,13 +415,9 @@ static cudaError_t plan_impl(int n_frames, int n_data, FusedLaunch* l) {
 
 template <int M, bool ZF, bool BPSK>
 static cudaError_t launch_one(const FusedParams& p, const FusedLaunch& l, cudaStream_t s) {
-  static bool attr_set = false;  // benign race: idempotent attribute write
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rx_fused_kernel<M, ZF, BPSK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static unsigned attr_done = 0;
+  if (cudaError_t e = ensure_smem_attr(rx_fused_kernel<M, ZF, BPSK>, 227 * 1024, attr_done); e != cudaSuccess)
+    return e;
   if (l.grid == 0) return cudaSuccess;
   rx_fused_kernel<M, ZF, BPSK><<<l.grid, l.threads, l.smem, s>>>(p);
   return cudaGetLastError();

@@ -52,12 +52,8 @@ static cudaError_t fft_rows_impl(const FftRowsParams& p, cudaStream_t s) {
   const int lanes = G >= 256 ? 1 : 256 / G;
   const int threads = lanes * G;
   const size_t smem = (size_t)lanes * PI::SLOT * sizeof(float2);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fft_rows_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static unsigned attr_done = 0;
+  if (cudaError_t e = ensure_smem_attr(fft_rows_kernel<M>, 227 * 1024, attr_done); e != cudaSuccess) return e;
   const long long rows = (long long)p.n_frames * p.n_sym * p.n_ant;
   if (rows == 0) return cudaSuccess;
   long long blocks = (rows + lanes - 1) / lanes;

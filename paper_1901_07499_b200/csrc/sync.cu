@@ -382,12 +382,8 @@ cudaError_t launch_corr_fft(const SyncParams& p, float2* cspec, int bound_mode, 
   using PI = PlanInfo<CF_N>;
   const size_t smem = (size_t)CF_LANES * (PI::SLOT * sizeof(float2) + (CF_N + 4) * sizeof(float)) +
                       CF_N * sizeof(float2);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(corr_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static unsigned attr_done = 0;
+  if (cudaError_t e = ensure_smem_attr(corr_fft_kernel, (int)smem, attr_done); e != cudaSuccess) return e;
   if (p.keys != nullptr) {
     cudaError_t e = cudaMemsetAsync(p.keys, 0, (size_t)p.n_frames * p.n_ant * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
@@ -409,14 +405,9 @@ size_t sync_smem_bytes(int n_chips) { return (size_t)(2 * n_chips - 1 + SYNC_TW 
 cudaError_t launch_corr(const SyncParams& p, cudaStream_t s) {
   if ((long long)p.n_frames * p.n_ant == 0 || p.wins <= 0) return cudaSuccess;
   const size_t smem = sync_smem_bytes(p.n_chips);
-  static bool attr_set = false;
-  if (!attr_set) {
-    // enough for the largest PN the ABI accepts (8192 chips)
-    cudaError_t e = cudaFuncSetAttribute(corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sync_smem_bytes(8192));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static unsigned attr_done = 0;  // enough for the largest PN the ABI accepts (8192 chips)
+  if (cudaError_t e = ensure_smem_attr(corr_kernel, (int)sync_smem_bytes(8192), attr_done); e != cudaSuccess)
+    return e;
   if (p.keys != nullptr) {
     cudaError_t e = cudaMemsetAsync(p.keys, 0, (size_t)p.n_frames * p.n_ant * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;

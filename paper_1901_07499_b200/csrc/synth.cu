@@ -206,12 +206,8 @@ cudaError_t tx_impl(const SynthParams& p, cudaStream_t s) {
   constexpr int G = PI::G;
   const int lanes = G >= 256 ? 1 : 256 / G;
   const size_t smem = (size_t)lanes * PI::SLOT * sizeof(float2);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tx_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static unsigned attr_done = 0;
+  if (cudaError_t e = ensure_smem_attr(tx_kernel<M>, 227 * 1024, attr_done); e != cudaSuccess) return e;
   const long long rows = (long long)p.n_frames * (1 + p.n_data);
   tx_kernel<M><<<(unsigned)((rows + lanes - 1) / lanes), lanes * G, smem, s>>>(p, lanes);
   return cudaGetLastError();
