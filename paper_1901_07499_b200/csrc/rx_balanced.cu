@@ -83,12 +83,10 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
     mbar_arrive_expect_tx(bar, bytes);
     tma_bulk_g2s(slot_base + (size_t)st * BSS, reinterpret_cast<const void*>(start), bytes, bar, pol);
   };
-  uint32_t rx_phase[2] = {0u, 0u};
   uint32_t h_phase = 0u;
-  auto wait_rx = [&](int st) {
-    mbar_wait_parity(&rx_bar[2 * w + st], rx_phase[st]);
-    rx_phase[st] ^= 1u;
-  };
+  // stage st = k & 1 is used at every other step, so its phase is (k >> 1) & 1
+  // (a per-stage phase array indexed by st would live in local memory)
+  auto wait_rx = [&](int kk) { mbar_wait_parity(&rx_bar[2 * w + (kk & 1)], (uint32_t)(kk >> 1) & 1u); };
 
   // ---------------- phase A: pilot rows --------------------------------------
   uint32_t pmask = 0;
@@ -116,7 +114,7 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
       if (n + BW < N) issue_rx(row_addr(0, n + BW), st ^ 1);
       else if (r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), st ^ 1);  // first data row of phase B
     }
-    wait_rx(st);
+    wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(0, n)) >> 3) & 1);
     const float2* src = slot + sh;
     fft_forward<BM>(v, slot, t, [&](int idx) { return src[idx]; }, [] { __syncwarp(); });
@@ -161,7 +159,7 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
     const int st = k & 1;
     float2* slot = slot_base + (size_t)st * BSS;
     if (leader && r + 1 < r1) issue_rx(row_addr(1 + dn, nn), st ^ 1);
-    wait_rx(st);
+    wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(1 + d, n)) >> 3) & 1);
     const float2* src = slot + sh;
 #ifdef OFDMRX_BAL_H_TMA
