@@ -69,8 +69,6 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
   const uint32_t tbase = *tmem_slot + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * BCOLS);
   const uint32_t t_den = tbase + 2 * BACC;
 
-  uint64_t pol = 0;
-  if (leader) pol = l2_evict_first_policy();
   const float2* frame = p.rx + (long long)f * p.frame_stride + p.sym0 + p.cp;
   float2* Hf = p.H + (long long)f * N * BM;
   // rx row (symbol s, antenna n): TMA into stage st of this warp
@@ -81,7 +79,9 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
     const uint32_t bytes = (uint32_t)(((a + (uintptr_t)BM * 8u + 15u) & ~uintptr_t(15)) - start);
     uint64_t* bar = &rx_bar[2 * w + st];
     mbar_arrive_expect_tx(bar, bytes);
-    tma_bulk_g2s(slot_base + (size_t)st * BSS, reinterpret_cast<const void*>(start), bytes, bar, pol);
+    // policy made at the issue (1 instruction) rather than held in 2 registers
+    tma_bulk_g2s(slot_base + (size_t)st * BSS, reinterpret_cast<const void*>(start), bytes, bar,
+                 l2_evict_first_policy());
   };
   uint32_t h_phase = 0u;
   // stage st = k & 1 is used at every other step, so its phase is (k >> 1) & 1
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
                       __syncwarp();
                       if (leader) {
                         mbar_arrive_expect_tx(&h_bar[w], BM * 8u);
-                        tma_bulk_g2s(slot, Hf + (long long)n * BM, BM * 8u, &h_bar[w], pol);
+                        tma_bulk_g2s(slot, Hf + (long long)n * BM, BM * 8u, &h_bar[w], l2_evict_first_policy());
                       }
                     });
     const uint32_t tacc = tbase + (uint32_t)((d - d_first) * BACC);
