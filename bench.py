@@ -410,14 +410,19 @@ def run_b200(args, cfg_name, world, rank, local):
     peak, peak_kind = load_peaks()
     bpf = frame_bytes(n // (world if sharded is not None else 1), m, qam, d)
     achieved = bpf * F / (kernel_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_detail = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg_name}.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
-        traffic = tj["dram_bytes_per_frame"] * F / (kernel_ms * 1e-3) / 1e9 if "dram_bytes_per_frame" in tj else None
-        traffic = {"dram_bytes_per_launch": int(tj["dram_bytes_per_frame"] * F), "as_gbs": traffic,
-                   "source": tj.get("source")} if traffic else None
+        if "dram_bytes_per_frame" in tj:
+            # same units as `achieved`: the ncu-measured DRAM bytes of one launch
+            # of this size over the live kernel time
+            traffic = tj["dram_bytes_per_frame"] * F / (kernel_ms * 1e-3) / 1e9
+            traffic_detail = {"dram_bytes_per_launch": int(tj["dram_bytes_per_frame"] * F),
+                              "algorithmic_bytes_per_launch": int(frame_bytes(n // (world if sharded is not None else 1),
+                                                                              m, qam, d) * F),
+                              "source": tj.get("source")}
 
     line = {
         "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
@@ -433,7 +438,7 @@ def run_b200(args, cfg_name, world, rank, local):
                    if x.numel() * 8 > 126e6 else "inputs smaller than L2"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_kind,
+                     "traffic": traffic, "traffic_detail": traffic_detail, "peak_source": peak_kind,
                      "bytes_per_frame": bpf, "kernel_ms": kernel_ms},
         "clocks": clocks.summary(),
         "check": {"ber_vs_tx": ber, "flagged_frames": flags_bad},

@@ -23,7 +23,7 @@ wr = d["dram__bytes_write.sum"][0] * scale[d["dram__bytes_write.sum"][1]]
 dur = d["gpu__time_duration.sum"][0] * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3}[d["gpu__time_duration.sum"][1]]
 out = {"dram_bytes_per_frame": (rd + wr) / frames, "dram_read_bytes": rd, "dram_write_bytes": wr,
        "frames_in_launch": frames, "ncu_duration_s": dur, "source": label,
-       "note": "ncu --set full --clock-control none, one rx_fused launch; writes still resident in L2 at "
+       "note": "ncu --set full --clock-control none, one launch of the product kernel; writes still resident in L2 at "
                "kernel end are not counted by dram__bytes_write"}
 json.dump(out, open(f"profiles/traffic_{cfg}.json", "w"), indent=1)
 print(out)
