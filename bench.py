@@ -56,20 +56,36 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host receipt time, csv line)
+        self.window = None
+
+    def mark(self, t0, t1):
+        """Host wall-clock (time.time()) bounds of the timed region: only
+        samples nvidia-smi timestamped inside it enter the summary (idle
+        samples would mask a power cap)."""
+        self.window = (t0, t1)
+
+    @staticmethod
+    def _stamp(text):
+        import datetime
+
+        try:
+            return datetime.datetime.strptime(text.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -78,7 +94,8 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            line = line.strip()
+            self.lines.append((self._stamp(line.split(",")[0]), line))
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -89,12 +106,24 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
+        lines = self.lines
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [x for x in lines if x[0] is not None and t0 <= x[0] <= t1]
+            if not inside:  # region shorter than the period: the first sample after it started
+                inside = [x for x in lines if x[0] is not None and x[0] >= t0][:1]
+            lines = inside
+        for _, line in lines:
+            parts = [p.strip() for p in line.split(",")][1:]  # drop the timestamp
             if len(parts) < 6:
                 continue
+            if len(parts) > 6:
+                try:
+                    power.append(float(parts[6].split()[0]))
+                except (ValueError, IndexError):
+                    pass
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
@@ -105,7 +134,11 @@ class ClockSampler:
                     reasons.add(name)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+               "window": "timed region only" if self.window is not None else "whole sampler run"}
+        if power:
+            out["power_w_median"] = statistics.median(power)
+        return out
 
 
 def dist_setup(n_gpus):
@@ -381,17 +414,21 @@ def run_b200(args, cfg_name, world, rank, local):
     idx = np.arange(lo, hi)
     ber = float((out.bits[lo:hi].cpu().numpy() != bits_truth[idx % len(bits_truth)]).mean())
     flags_bad = int((out.flags != 0).sum())
-    for _ in range(max(0, args.warmup - 1)):
-        step()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
-        time.sleep(0.3)
+        time.sleep(0.3)  # sampler running before the warm-up
+        # the warm-up steps run right before the timed region: an idle gap here
+        # lets the SM clock drop and the first timed launches pay the ramp
+        for _ in range(max(0, args.warmup - 1)):
+            step()
+        torch.cuda.synchronize()
         barrier(world)
         torch.cuda.synchronize()
         t_start = torch.cuda.Event(enable_timing=True)
         t_stop = torch.cuda.Event(enable_timing=True)
+        h0 = time.time()
         t_start.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
@@ -399,6 +436,8 @@ def run_b200(args, cfg_name, world, rank, local):
             ev[i][1].record(stream)
         t_stop.record(stream)
         torch.cuda.synchronize()
+        clocks.mark(h0, time.time())
+        time.sleep(0.25)  # let nvidia-smi deliver the samples it took inside the window
         barrier(world)
     total_ms = t_start.elapsed_time(t_stop)
     kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
