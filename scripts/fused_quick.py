@@ -19,6 +19,7 @@ cfg_name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 n, m, cp, qam, d, F = bench.CONFIGS[cfg_name]
 if len(sys.argv) > 2:
     F = int(sys.argv[2])
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
 cfg, rx, bits, s0 = bench.make_inputs(cfg_name)
 x = torch.from_numpy(rx).cuda().repeat((F + len(rx) - 1) // len(rx), 1, 1)[:F].contiguous()
 out = frames.allocate_outputs(F, n, m, d, qam, x.device)
@@ -27,7 +28,6 @@ for _ in range(3):
 torch.cuda.synchronize()
 ber = float((out.bits[:len(rx)].cpu().numpy() != bits[:min(len(rx), F)]).mean())
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-reps = 20
 a.record()
 for _ in range(reps):
     frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out)
@@ -36,5 +36,5 @@ torch.cuda.synchronize()
 ms = a.elapsed_time(b) / reps
 peak, _ = bench.load_peaks()
 bpf = bench.frame_bytes(n, m, qam, d)
-print(json.dumps({"lib": os.environ.get("OFDMRX_LIB", "in-tree"), "cfg": cfg_name, "frames": F, "ms": ms,
+print(json.dumps({"lib": os.environ.get("OFDMRX_LIB", "in-tree"), "cfg": cfg_name, "frames": F, "reps": reps, "ms": ms,
                   "us_per_frame": ms * 1e3 / F, "frac": bpf * F / (ms * 1e-3) / 1e9 / peak, "ber": ber}))
