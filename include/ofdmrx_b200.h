@@ -54,6 +54,8 @@ typedef enum {
 /* Per-frame flag bits written by the fused / finish kernels (atomic OR). */
 #define OFDMRX_FLAG_NONFINITE 1u /* a non-finite sample reached the FFT: to_freq raises NumericInputError (receiver.py:202-203) */
 #define OFDMRX_FLAG_ERASED 2u    /* some subcarrier weight < eps: CombinedSymbol.erased (receiver.py:234) */
+#define OFDMRX_FLAG_NOT_DETECTED 4u /* ofdmrx_rx_frames_detected: antenna-0 peak below threshold (DetectionResult.detected false, sync.py:40); frame skipped */
+#define OFDMRX_FLAG_OUT_OF_RANGE 8u /* ofdmrx_rx_frames_detected: the detected frame overruns the capture (extract_slots InputError, receiver.py:278-283); frame skipped */
 
 /*
  * Batch of F captures, each N antenna rows of samples.  Frame f, antenna n,
@@ -110,6 +112,22 @@ OFDMRX_API int ofdmrx_check_desc(const ofdmrx_frame_desc* desc, int64_t rx_len_s
  */
 OFDMRX_API int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
                      float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream);
+
+/*
+ * ofdmrx_rx_frames with each frame's symbol0 taken from a device-side
+ * detection (ofdmrx_detect outputs, no host round trip): symbol0 of frame f
+ * = peak_index[f * peak_stride] + n_chips (DetectionResult.symbol0_offset,
+ * sync.py:37-42, antenna 0).  desc.symbol0_offset must be 0; rows hold
+ * n_samples samples.  Frames with peak_metric[f * peak_stride] < threshold
+ * get OFDMRX_FLAG_NOT_DETECTED, frames whose 1 + D symbols overrun the row get
+ * OFDMRX_FLAG_OUT_OF_RANGE; both are skipped (their outputs unspecified).
+ * flags is required.  This is the reference's detect_packet -> extract_slots
+ * -> run_ring_pipeline chain (cli.py:306-321) for F captures in two launches.
+ */
+OFDMRX_API int ofdmrx_rx_frames_detected(const ofdmrx_frame_desc* desc, int64_t n_samples, const int32_t* peak_index,
+                                         const double* peak_metric, int32_t peak_stride, int32_t n_chips,
+                                         double threshold, const void* rx, const void* pilot, void* H, void* s_hat,
+                                         float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream);
 
 /*
  * Antenna-sharded variant, step 1: the same fused pass over this shard's

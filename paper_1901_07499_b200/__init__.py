@@ -27,7 +27,7 @@ def __getattr__(name):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)
-    if name in ("receive_frames", "receive_partials", "finish_partials", "FrameBatch"):
+    if name in ("receive_frames", "receive_partials", "finish_partials", "FrameBatch", "receive_captures"):
         from . import frames
 
         return getattr(frames, name)

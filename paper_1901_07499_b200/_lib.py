@@ -24,6 +24,8 @@ ABI_VERSION = 1
 OK, ERR_CONFIG, ERR_CONTRACT, ERR_INPUT, ERR_NUMERIC, ERR_CUDA = range(6)
 FLAG_NONFINITE = 1
 FLAG_ERASED = 2
+FLAG_NOT_DETECTED = 4
+FLAG_OUT_OF_RANGE = 8
 OPT_PILOT_BPSK = 1
 OPT_NO_SHARDS = 2
 
@@ -102,6 +104,8 @@ SIGNATURES = {
     "ofdmrx_synth_rayleigh": (ctypes.c_int, [_p, _i32, ctypes.c_uint64, _p]),
     "ofdmrx_synth_frames": (ctypes.c_int, [_SDESC, _p, _p, _p, _p, _p, _p]),
     "ofdmrx_rx_partials_routed": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _i32, _i32, _p, _p]),
+    "ofdmrx_rx_frames_detected": (ctypes.c_int, [_DESC, _i64, _p, _p, _i32, _i32, ctypes.c_double, _p, _p, _p, _p, _p,
+                                                 _p, _p, _p, _p]),
     "ofdmrx_peer_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(ctypes.c_void_p), _p]),
     "ofdmrx_peer_open": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_void_p)]),
     "ofdmrx_peer_close": (ctypes.c_int, [_p]),

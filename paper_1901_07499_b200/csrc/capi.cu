@@ -133,6 +133,14 @@ int scratch_alloc(void** ptr, size_t bytes, cudaStream_t st) {
   return OFDMRX_OK;
 }
 
+struct Detected {  // per-frame symbol0 from ofdmrx_detect outputs
+  const int32_t* idx;
+  const double* metric;
+  int stride, add;
+  double threshold;
+  long long n_samples;
+};
+
 struct Route {  // partial sums routed to the owners' peer inboxes
   const void* num_dst;
   const void* den_dst;
@@ -141,7 +149,7 @@ struct Route {  // partial sums routed to the owners' peer inboxes
 
 int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, int mode, void* H, void* s_hat,
                  float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream,
-                 const Route* route = nullptr) {
+                 const Route* route = nullptr, const Detected* det = nullptr) {
   if (int rc = check_desc_impl(d, -1)) return rc;
   if (d->n_frames == 0) return OFDMRX_OK;
   if (int rc = check_ptr(rx, "rx")) return rc;
@@ -206,6 +214,14 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   p.flags = flags;
   p.part_num = static_cast<float2*>(num);
   p.part_den = den;
+  if (det != nullptr) {
+    p.det_idx = det->idx;
+    p.det_metric = det->metric;
+    p.det_stride = det->stride;
+    p.det_add = det->add;
+    p.det_threshold = det->threshold;
+    p.n_samples = det->n_samples;
+  }
   if (route != nullptr) {
     p.num_dst = static_cast<float2* const*>(route->num_dst);
     p.den_dst = static_cast<float* const*>(route->den_dst);
@@ -370,6 +386,26 @@ int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* 
 int ofdmrx_rx_partials(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* num,
                        float* den, uint32_t* flags, void* stream) {
   return fused_common(desc, rx, pilot, 1, H, nullptr, nullptr, nullptr, nullptr, flags, num, den, stream);
+}
+
+int ofdmrx_rx_frames_detected(const ofdmrx_frame_desc* desc, int64_t n_samples, const int32_t* peak_index,
+                              const double* peak_metric, int32_t peak_stride, int32_t n_chips, double threshold,
+                              const void* rx, const void* pilot, void* H, void* s_hat, float* weights, uint8_t* bits,
+                              void* zf, uint32_t* flags, void* stream) {
+  if (desc == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
+  if (desc->symbol0_offset != 0)
+    return fail(OFDMRX_ERR_CONTRACT, "symbol0_offset must be 0: it comes from peak_index per frame");
+  if (n_chips < 0 || peak_stride < 1) return fail(OFDMRX_ERR_CONTRACT, "need n_chips >= 0 and peak_stride >= 1");
+  if (n_samples < (long long)(1 + desc->n_data) * (desc->fft_len + desc->cp_len))
+    return fail(OFDMRX_ERR_INPUT, "rows of %lld samples cannot hold %d symbols", (long long)n_samples,
+                1 + desc->n_data);
+  if (desc->n_frames > 0) {
+    if (int rc = check_ptr(peak_index, "peak_index")) return rc;
+    if (int rc = check_ptr(peak_metric, "peak_metric")) return rc;
+    if (int rc = check_ptr(flags, "flags")) return rc;  // rejected frames are only visible here
+  }
+  const Detected det{peak_index, peak_metric, peak_stride, n_chips, threshold, n_samples};
+  return fused_common(desc, rx, pilot, 0, H, s_hat, weights, bits, zf, flags, nullptr, nullptr, stream, nullptr, &det);
 }
 
 int ofdmrx_rx_partials_routed(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H,

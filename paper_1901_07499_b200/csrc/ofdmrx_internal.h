@@ -55,7 +55,25 @@ struct FusedParams {
   float2* const* num_dst;
   float* const* den_dst;
   int fpo, slot;
+  // per-frame symbol0 from a device-side detection (ofdmrx_rx_frames_detected):
+  // sym0_f = det_idx[f * det_stride] + det_add; frames whose antenna-0 peak is
+  // below det_threshold, or whose symbols overrun n_samples, are flagged and skipped
+  const int32_t* det_idx;
+  const double* det_metric;
+  int det_stride, det_add;
+  double det_threshold;
+  long long n_samples;
 };
+
+// per-frame symbol0 (detected or fixed) and the frame's admission flags
+__device__ __forceinline__ long long frame_sym0(const FusedParams& p, int f, int M, uint32_t* reject) {
+  *reject = 0u;
+  if (p.det_idx == nullptr) return p.sym0;
+  const long long s0 = (long long)p.det_idx[(long long)f * p.det_stride] + p.det_add;
+  if (!(p.det_metric[(long long)f * p.det_stride] >= p.det_threshold)) *reject |= 4u;  // OFDMRX_FLAG_NOT_DETECTED
+  if (s0 + (long long)(1 + p.n_data) * (M + p.cp) > p.n_samples) *reject |= 8u;       // OFDMRX_FLAG_OUT_OF_RANGE
+  return *reject ? 0 : s0;
+}
 
 struct FusedLaunch {
   int dc, n_chunks, fpb, lanes, threads, grid, ngroups, npilot;

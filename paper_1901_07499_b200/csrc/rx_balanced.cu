@@ -54,6 +54,12 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
   const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
   const int f = blockIdx.x;
   const int N = p.n_ant, D = p.n_data;
+  uint32_t reject = 0u;
+  const long long sym0 = frame_sym0(p, f, BM, &reject);
+  if (reject != 0u) {  // not detected / out of range: flagged, no traffic, no outputs
+    if (threadIdx.x == 0 && p.flags != nullptr) atomicOr(&p.flags[f], reject);
+    return;
+  }
   uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [BW][2]
   uint64_t* h_bar = rx_bar + 2 * BW;                          // [BW]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_bar + BW);
@@ -69,7 +75,7 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
   const uint32_t tbase = *tmem_slot + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * BCOLS);
   const uint32_t t_den = tbase + 2 * BACC;
 
-  const float2* frame = p.rx + (long long)f * p.frame_stride + p.sym0 + p.cp;
+  const float2* frame = p.rx + (long long)f * p.frame_stride + sym0 + p.cp;
   float2* Hf = p.H + (long long)f * N * BM;
   // rx row (symbol s, antenna n): TMA into stage st of this warp
   auto row_addr = [&](int s, int n) { return frame + (long long)n * p.row_stride + (long long)s * (BM + p.cp); };

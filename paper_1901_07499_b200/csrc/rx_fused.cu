@@ -95,13 +95,19 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   const int lane = unit * GI + sub;
   const int warp = threadIdx.x >> 5;
   const int work = blockIdx.x * p.fpb + grp * GI + sub;
-  const bool item_ok = work < p.n_work;
+  bool item_ok = work < p.n_work;
   // work = (frame, chunk, antenna shard), shards innermost
   const int shard = item_ok ? work % p.n_shards : 0;
   const int fc = item_ok ? work / p.n_shards : 0;
   const int f = fc / p.n_chunks;
   const int chunk = fc - f * p.n_chunks;
   const int ant0 = shard * p.n_ant;  // first antenna of this shard (global index)
+  uint32_t reject = 0u;
+  const long long sym0 = item_ok ? frame_sym0(p, f, M, &reject) : p.sym0;
+  if (reject != 0u) {  // not detected / out of range: flagged, no traffic, no outputs
+    if (sl == 0 && t == 0 && chunk == 0 && shard == 0 && p.flags != nullptr) atomicOr(&p.flags[f], reject);
+    item_ok = false;
+  }
   const bool is_pilot = sl < npilot;
   const int d = is_pilot ? 0 : chunk * p.dc + (sl - npilot);  // data-symbol index (0-based)
   const bool active = item_ok && (is_pilot || d < p.n_data);
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     else named_bar_sync(1 + unit, UT);
   };
 
-  const float2* row0 = p.rx + (long long)f * p.frame_stride + (long long)ant0 * p.row_stride + p.sym0 +
+  const float2* row0 = p.rx + (long long)f * p.frame_stride + (long long)ant0 * p.row_stride + sym0 +
                        (long long)s * (M + p.cp) + p.cp;
 
   if (threadIdx.x == 0) {

@@ -181,3 +181,45 @@ def test_batched_frames_feed_receive(S):
                                     symbol0_offset=int(det.symbol0_offset[i]), n_data=d)
         ref = orc.receive_frame(st, offs[i] + 255, m, cp, d, qam)[3]
         assert np.array_equal(out.bits[0].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("m,cp,n_ant,qam,d,shards", [(1024, 72, 16, 16, 4, False), (1024, 72, 16, 16, 4, True),
+                                                     (256, 32, 8, 16, 6, True), (64, 16, 4, 4, 10, False)])
+def test_receive_captures_device_timing(S, m, cp, n_ant, qam, d, shards):
+    """Raw captures with different timing offsets -> detect_frames ->
+    ofdmrx_rx_frames_detected (per-frame symbol0 on the device): every
+    detected frame decodes as the oracle at its true offset; a noise-only
+    capture is flagged NOT_DETECTED and a truncated one OUT_OF_RANGE."""
+    import paper_1901_07499_b200 as P
+    from paper_1901_07499_b200 import _lib, frames
+
+    pn = orc.generate_pn()
+    offs = [0, 37, 250, 501]
+    frame_len = 255 + (1 + d) * (m + cp)
+    s_len = frame_len + 520
+    rng = np.random.default_rng(m + d)
+    caps = []
+    for i, off in enumerate(offs):
+        bits = rng.integers(0, 2, size=d * m * int(np.log2(qam)), dtype=np.uint8)
+        samples, _, _ = orc.build_frame_samples(m, cp, qam, orc.make_pilot(m), bits, pn)
+        st, _ = orc.apply_channel(samples, n_ant, mode="flat_rayleigh", snr_db=12.0, timing_offset=off, rng_seed=i)
+        full = np.zeros((n_ant, s_len), dtype=np.complex128)
+        full[:, :st.shape[1]] = st
+        caps.append(full)
+    caps.append(0.5 * (rng.standard_normal((n_ant, s_len)) + 1j * rng.standard_normal((n_ant, s_len))))  # noise only
+    late = np.zeros((n_ant, s_len), dtype=np.complex128)  # packet starting too late to fit
+    late[:, s_len - 400:] = caps[0][:, :400]
+    caps.append(late)
+    batch = np.stack(caps)
+    cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    out, det = frames.receive_captures(torch.from_numpy(batch.astype(np.complex64)).cuda(), cfg, d, shards=shards)
+    torch.cuda.synchronize()
+    fl = out.flags.cpu().numpy()
+    for i, off in enumerate(offs):
+        assert int(det.frame_start[i]) == off and fl[i] == 0
+        H, s_hat, w, bits = orc.receive_frame(caps[i].astype(np.complex64).astype(np.complex128), off + 255, m, cp, d,
+                                              qam)
+        assert np.array_equal(out.bits[i].cpu().numpy(), bits)
+        assert np.linalg.norm(out.s_hat[i].cpu().numpy() - s_hat) / np.linalg.norm(s_hat) < 1e-4
+    assert fl[len(offs)] & _lib.FLAG_NOT_DETECTED
+    assert fl[len(offs) + 1] & _lib.FLAG_OUT_OF_RANGE
