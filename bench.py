@@ -643,7 +643,14 @@ def run_sync_stage(cfg, d, Fs, timed):
     t, det = timed(lambda: sync.detect_frames(x, pn))
     ok = bool((det.frame_start == 0).all()) and bool((det.symbol0_offset == pn.size).all())
     rows, wins = Fs * cfg.n_antennas, x.shape[2] - pn.size + 1
-    return {"frames": Fs, "samples_per_row": int(x.shape[2]), "us_per_frame": t / Fs,
+    from paper_1901_07499_b200 import frames
+
+    # the whole device pipeline on raw captures: detection -> per-frame timing -> fused receive
+    tp, (outp, detp) = timed(lambda: frames.receive_captures(x, cfg, d, pn))
+    pipe = {"us_per_frame": tp / Fs, "symbols_per_s": Fs * (1 + d) / (tp * 1e-6),
+            "flagged_frames": int((outp.flags != 0).sum()),
+            "path": "frames.receive_captures: ofdmrx_detect + ofdmrx_rx_frames_detected, no host round trip"}
+    return {"frames": Fs, "samples_per_row": int(x.shape[2]), "us_per_frame": t / Fs, "pipeline": pipe,
             "cmac_per_s": rows * wins * pn.size / (t * 1e-6), "all_offsets_found": ok,
             "path": "ofdmrx_detect: fp32 corr_kernel (FFMA2) + fp64 refine of near-max windows"}
 

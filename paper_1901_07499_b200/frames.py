@@ -303,7 +303,7 @@ def _slice_batch(out, n):
 
 
 def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, eps=device.MRC_WEIGHT_FLOOR,
-                     want_h=True, zf=False, shards=True, stream=None):
+                     want_h=True, zf=False, shards=True, antennas="first", stream=None):
     """Raw captures -> bits with the packet timing found on the device.
 
     The reference's detect_packet -> extract_slots -> run_ring_pipeline chain
@@ -312,7 +312,9 @@ def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, ep
     the fused receive with each frame's symbol0 = its antenna-0 peak + PN
     length.  Frames whose peak is below `threshold` get FLAG_NOT_DETECTED,
     frames too short for 1 + n_data symbols after the peak FLAG_OUT_OF_RANGE;
-    both are skipped.  Returns (FrameBatch, FrameDetections)."""
+    both are skipped.  The decision only needs antenna 0 (sync.py:37-42), so
+    by default only antenna 0 is correlated (antennas="all" also reports every
+    antenna's peak).  Returns (FrameBatch, FrameDetections)."""
     from . import sync
     from .synth import generate_pn_chips
 
@@ -327,14 +329,15 @@ def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, ep
         raise ContractError(f"rx has {n} antenna rows, config has {cfg.n_antennas}")
     chips = generate_pn_chips(length=cfg.pn_len) if pn is None else pn
     thr = sync.DEFAULT_THRESHOLD if threshold is None else float(threshold)
-    det = sync.detect_frames(x, chips, thr, stream=stream)
+    det = sync.detect_frames(x, chips, thr, antennas=antennas, stream=stream)
     pvals = _pilot_values(pilot, cfg.fft_len)
     desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, 0, s, n * s, eps,
                             options=device.pilot_options(pvals) | (0 if shards else _lib.OPT_NO_SHARDS))
     pv = _PILOTS.get(pvals, dev)
     out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
     _lib.call("ofdmrx_rx_frames_detected", ctypes.byref(desc), s, device.ptr(det.peak_index),
-              device.ptr(det.peak_metric), n, det.n_chips, thr, device.ptr(x), device.ptr(pv), device.ptr(out.H),
+              device.ptr(det.peak_metric), det.peak_index.shape[1], det.n_chips, thr, device.ptr(x), device.ptr(pv),
+              device.ptr(out.H),
               device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
               device.ptr(out.flags), device.stream_handle(stream))
     return out, det

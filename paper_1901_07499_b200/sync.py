@@ -109,28 +109,34 @@ def _rows(rx, dev):
     return x
 
 
-def detect_frames(rx, pn, threshold=DEFAULT_THRESHOLD, *, scratch=None, stream=None):
-    """Detect the PN preamble in every antenna stream of F captures.
+def detect_frames(rx, pn, threshold=DEFAULT_THRESHOLD, *, antennas="all", scratch=None, stream=None):
+    """Detect the PN preamble in the antenna streams of F captures.
 
     rx: complex64 CUDA tensor [F, N, S] (or [N, S]; numpy is copied H2D).
     pn: PnSequence-like (``.chips``) or a real chip array.
+    antennas: "all" (every antenna's peak, DetectionResult.per_antenna_peaks)
+    or "first" (antenna 0 only: the decision input of sync.py:37-42, 1/N of
+    the work; peak arrays are then [F, 1]).
     Returns FrameDetections (no host sync)."""
+    if antennas not in ("all", "first"):
+        raise ContractError('antennas must be "all" or "first"')
     dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
     chips = _chips_of(pn)
     x = _rows(rx, dev)
     f, n, s = x.shape
     if s < chips.size:
         raise InputError(f"stream length {s} shorter than PN length {chips.size}")  # sync.py:28-31
+    n_rows = n if antennas == "all" else 1  # antenna 0 only: rows f*N*S, one per frame
     lib = _lib.load()
-    need = int(lib.ofdmrx_detect_scratch_bytes(f, n, s, int(chips.size)))
+    need = int(lib.ofdmrx_detect_scratch_bytes(f, n_rows, s, int(chips.size)))
     if need < 0:
         raise ContractError("invalid detection sizes")
     if scratch is None or scratch.numel() < need:
         scratch = torch.empty((max(need, 8),), dtype=torch.uint8, device=dev)
-    idx = torch.empty((f, n), dtype=torch.int32, device=dev)
-    met = torch.empty((f, n), dtype=torch.float64, device=dev)
+    idx = torch.empty((f, n_rows), dtype=torch.int32, device=dev)
+    met = torch.empty((f, n_rows), dtype=torch.float64, device=dev)
     c = _CHIPS.get(chips, dev)
-    _lib.call("ofdmrx_detect", device.ptr(x), f, n, s, s, n * s, device.ptr(c), int(chips.size),
+    _lib.call("ofdmrx_detect", device.ptr(x), f, n_rows, s, s, n * s, device.ptr(c), int(chips.size),
               device.ptr(scratch), device.ptr(idx), device.ptr(met), device.stream_handle(stream))
     return FrameDetections(peak_index=idx, peak_metric=met, n_chips=int(chips.size), threshold=float(threshold))
 

@@ -183,9 +183,11 @@ def test_batched_frames_feed_receive(S):
         assert np.array_equal(out.bits[0].cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("m,cp,n_ant,qam,d,shards", [(1024, 72, 16, 16, 4, False), (1024, 72, 16, 16, 4, True),
-                                                     (256, 32, 8, 16, 6, True), (64, 16, 4, 4, 10, False)])
-def test_receive_captures_device_timing(S, m, cp, n_ant, qam, d, shards):
+@pytest.mark.parametrize("m,cp,n_ant,qam,d,shards,ants", [(1024, 72, 16, 16, 4, False, "first"),
+                                                          (1024, 72, 16, 16, 4, True, "all"),
+                                                          (256, 32, 8, 16, 6, True, "first"),
+                                                          (64, 16, 4, 4, 10, False, "all")])
+def test_receive_captures_device_timing(S, m, cp, n_ant, qam, d, shards, ants):
     """Raw captures with different timing offsets -> detect_frames ->
     ofdmrx_rx_frames_detected (per-frame symbol0 on the device): every
     detected frame decodes as the oracle at its true offset; a noise-only
@@ -212,7 +214,9 @@ def test_receive_captures_device_timing(S, m, cp, n_ant, qam, d, shards):
     caps.append(late)
     batch = np.stack(caps)
     cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
-    out, det = frames.receive_captures(torch.from_numpy(batch.astype(np.complex64)).cuda(), cfg, d, shards=shards)
+    out, det = frames.receive_captures(torch.from_numpy(batch.astype(np.complex64)).cuda(), cfg, d, shards=shards,
+                                       antennas=ants)
+    assert det.peak_index.shape[1] == (n_ant if ants == "all" else 1)
     torch.cuda.synchronize()
     fl = out.flags.cpu().numpy()
     for i, off in enumerate(offs):
