@@ -23,7 +23,7 @@ from .waveform import OfdmConfig, PilotDefinition, default_cp, make_pilot  # noq
 
 def __getattr__(name):
     # heavy (torch) modules load lazily
-    if name in ("receiver", "frames", "device", "synth", "sharding", "sync"):
+    if name in ("receiver", "frames", "device", "synth", "sharding", "sync", "ingest"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)

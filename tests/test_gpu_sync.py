@@ -227,3 +227,31 @@ def test_receive_captures_device_timing(S, m, cp, n_ant, qam, d, shards, ants):
         assert np.linalg.norm(out.s_hat[i].cpu().numpy() - s_hat) / np.linalg.norm(s_hat) < 1e-4
     assert fl[len(offs)] & _lib.FLAG_NOT_DETECTED
     assert fl[len(offs) + 1] & _lib.FLAG_OUT_OF_RANGE
+
+
+def test_files_to_bits(S, tmp_path):
+    """Capture directories in the reference layout (rx_meta.txt +
+    rx_ant<k>.cf32, cli._load_capture) -> ingest.load_captures (pinned) ->
+    receive_captures on the device -> bits equal the oracle's."""
+    import paper_1901_07499_b200 as P
+    from paper_1901_07499_b200 import frames, ingest
+
+    m, cp, n_ant, qam, d = 256, 32, 8, 16, 5
+    cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    pn = orc.generate_pn()
+    dirs, truth = [], []
+    for i, off in enumerate((0, 77, 300)):
+        bits = np.random.default_rng(40 + i).integers(0, 2, size=d * m * 4, dtype=np.uint8)
+        samples, _, _ = orc.build_frame_samples(m, cp, qam, orc.make_pilot(m), bits, pn)
+        st, _ = orc.apply_channel(samples, n_ant, mode="flat_rayleigh", snr_db=12.0, timing_offset=off, rng_seed=i)
+        ingest.write_capture(str(tmp_path / f"cap{i}"), st, cfg)
+        dirs.append(str(tmp_path / f"cap{i}"))
+        truth.append((st.astype(np.complex64).astype(np.complex128), off))
+    metas, cfg2, host = ingest.load_captures(dirs, pinned=True)
+    assert host.is_pinned() and cfg2 == cfg
+    out, det = frames.receive_captures(host.cuda(non_blocking=True), cfg2, d)
+    torch.cuda.synchronize()
+    for i, (st, off) in enumerate(truth):
+        assert int(det.frame_start[i]) == off and int(out.flags[i]) == 0
+        H, s_hat, w, bits = orc.receive_frame(st, off + 255, m, cp, d, qam)
+        assert np.array_equal(out.bits[i].cpu().numpy(), bits)
