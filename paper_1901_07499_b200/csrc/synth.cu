@@ -39,16 +39,25 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+// SplitMix64 per (seed, stream): key once per stream, one finaliser per draw
+__device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t stream) {
+  return mix64(seed ^ mix64(stream * 0xD1B54A32D192ED03ull));
+}
+__device__ __forceinline__ uint64_t rng_draw(uint64_t key, uint64_t index) {
+  return mix64(key + index * 0x9E3779B97F4A7C15ull);
+}
 __device__ __forceinline__ uint64_t rng64(uint64_t seed, uint64_t stream, uint64_t index) {
-  return mix64(seed ^ mix64(stream * 0xD1B54A32D192ED03ull ^ mix64(index)));
+  return rng_draw(rng_key(seed, stream), index);
 }
 // two independent N(0,1) from one 64-bit draw (Box-Muller, 2 x 32-bit uniforms in (0,1))
 __device__ __forceinline__ float2 normal2(uint64_t h) {
   const float u1 = ((float)(uint32_t)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
   const float u2 = ((float)(uint32_t)(h & 0xffffffu) + 0.5f) * (1.0f / 16777216.0f);
-  const float r = sqrtf(-2.0f * logf(u1));
+  // fast intrinsics: ~2 ulp log / sin / cos on (0,1) x [0, 2pi) are far
+  // below what a noise generator needs
+  const float r = sqrtf(-2.0f * __logf(u1));
   float s, c;
-  sincospif(2.0f * u2, &s, &c);
+  __sincosf(6.283185307179586f * u2, &s, &c);
   return make_float2(r * c, r * s);
 }
 
@@ -148,17 +157,20 @@ __device__ __forceinline__ float2 signal_at(const SynthParams& p, long long f, i
   return acc;
 }
 
+// rows: (frame, antenna) with the channel response applied, or, for flat
+// channels (FLAT), frames only: |h|^2 * sum |tx|^2 is applied in channel_kernel
+template <bool FLAT>
 __global__ void __launch_bounds__(SIG_BLOCK) sigpow_kernel(const SynthParams p, int nblk) {
   const long long rowb = blockIdx.x;
   const long long row = rowb / nblk;
   const int b = (int)(rowb - row * nblk);
-  const long long f = row / p.n_ant;
-  const int n = (int)(row - f * p.n_ant);
+  const long long f = FLAT ? row : row / p.n_ant;
+  const int n = FLAT ? 0 : (int)(row - f * p.n_ant);
   const long long L = p.pn_len + p.tx_len;
   double e = 0.0;
   for (long long j = (long long)b * SIG_SPAN + threadIdx.x; j < L && j < (long long)(b + 1) * SIG_SPAN;
        j += SIG_BLOCK) {
-    const float2 y = signal_at(p, f, n, j);
+    const float2 y = FLAT ? tx_sample(p, f, j) : signal_at(p, f, n, j);
     e += (double)y.x * y.x + (double)y.y * y.y;
   }
   __shared__ double red[SIG_BLOCK];
@@ -173,26 +185,39 @@ __global__ void __launch_bounds__(SIG_BLOCK) sigpow_kernel(const SynthParams p, 
 
 constexpr int CH_SPAN = 2048;  // samples of one row per channel_kernel block
 
+template <bool FLAT>
 __global__ void __launch_bounds__(256) channel_kernel(const SynthParams p, int nblk, int spans) {
   const long long row = blockIdx.x / spans;  // (frame, antenna)
   const long long i0 = (long long)(blockIdx.x - row * spans) * CH_SPAN;
   const long long f = row / p.n_ant;
   const int n = (int)(row - f * p.n_ant);
   const long long L = p.pn_len + p.tx_len;
+  const float2 h0 = FLAT ? __ldg(p.resp + (p.resp_per_frame ? f * p.n_ant : 0) + n) : make_float2(1.f, 0.f);
   float sigma = 0.0f;
   if (p.noisy) {
     double e = 0.0;
-    for (int b = 0; b < nblk; ++b) e += p.sig_part[row * nblk + b];
+    const long long prow = FLAT ? f : row;
+    for (int b = 0; b < nblk; ++b) e += p.sig_part[prow * nblk + b];
+    if (FLAT) e *= (double)h0.x * h0.x + (double)h0.y * h0.y;  // mean |h tx|^2 = |h|^2 mean |tx|^2
     const double noise_power = (e / (double)L) / pow(10.0, (double)p.snr_db / 10.0);
     sigma = (float)sqrt(noise_power / 2.0);
   }
+  const uint64_t key = rng_key(p.seed, kStreamNoise + 16 * (uint64_t)row);
   float2* out = p.rx + row * p.n_samples;
   const long long i1 = i0 + CH_SPAN < p.n_samples ? i0 + CH_SPAN : p.n_samples;
   for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const long long j = i - p.offset;
-    float2 y = (j >= 0 && j < L) ? signal_at(p, f, n, j) : make_float2(0.f, 0.f);
+    float2 y = make_float2(0.f, 0.f);
+    if (j >= 0 && j < L) {
+      if constexpr (FLAT) {
+        const float2 x = tx_sample(p, f, j);
+        y = make_float2(fmaf(h0.x, x.x, -h0.y * x.y), fmaf(h0.x, x.y, h0.y * x.x));
+      } else {
+        y = signal_at(p, f, n, j);
+      }
+    }
     if (sigma > 0.0f) {
-      const float2 z = normal2(rng64(p.seed, kStreamNoise + 16 * (uint64_t)row, (uint64_t)i));
+      const float2 z = normal2(rng_draw(key, (uint64_t)i));
       y.x = fmaf(sigma, z.x, y.x);
       y.y = fmaf(sigma, z.y, y.y);
     }
@@ -247,12 +272,15 @@ cudaError_t launch_synth(const SynthParams& p, cudaStream_t s) {
   const long long L = p.pn_len + p.tx_len;
   const int nblk = (int)((L + SIG_SPAN - 1) / SIG_SPAN);
   const long long rows = (long long)p.n_frames * p.n_ant;
+  const bool flat = p.n_taps == 1;
   if (p.noisy) {
-    sigpow_kernel<<<(unsigned)(rows * nblk), SIG_BLOCK, 0, s>>>(p, nblk);
+    if (flat) sigpow_kernel<true><<<(unsigned)((long long)p.n_frames * nblk), SIG_BLOCK, 0, s>>>(p, nblk);
+    else sigpow_kernel<false><<<(unsigned)(rows * nblk), SIG_BLOCK, 0, s>>>(p, nblk);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   const int spans = (int)((p.n_samples + CH_SPAN - 1) / CH_SPAN);
-  channel_kernel<<<(unsigned)(rows * spans), 256, 0, s>>>(p, nblk, spans);
+  if (flat) channel_kernel<true><<<(unsigned)(rows * spans), 256, 0, s>>>(p, nblk, spans);
+  else channel_kernel<false><<<(unsigned)(rows * spans), 256, 0, s>>>(p, nblk, spans);
   return cudaGetLastError();
 }
 
