@@ -41,9 +41,6 @@ constexpr size_t BBAR = 512;             // mbarriers + TMEM address word
 
 __device__ __forceinline__ int range_lo(int w, int total) { return (int)((long long)total * w / BW); }
 
-__device__ __forceinline__ void mbar_arrive_b(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -89,7 +86,9 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
     tma_bulk_g2s(slot_base + (size_t)st * BSS, reinterpret_cast<const void*>(start), bytes, bar,
                  l2_evict_first_policy());
   };
+#ifdef OFDMRX_BAL_H_TMA
   uint32_t h_phase = 0u;
+#endif
   // stage st = k & 1 is used at every other step, so its phase is (k >> 1) & 1
   // (a per-stage phase array indexed by st would live in local memory)
   auto wait_rx = [&](int kk) { mbar_wait_parity(&rx_bar[2 * w + (kk & 1)], (uint32_t)(kk >> 1) & 1u); };

@@ -43,7 +43,7 @@ __device__ __forceinline__ const float2* row_ptr(const SyncParams& p, long long 
 }
 
 __global__ void __launch_bounds__(SYNC_THREADS) corr_kernel(const SyncParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int K = SYNC_K;
   const int P = p.n_chips;
   float2* cs = reinterpret_cast<float2*>(smem_raw);  // [P] (c, c)
