@@ -14,7 +14,6 @@ fp32 error bound of each row's maximum.
 [F, N, S]; its result feeds ``frames.receive_frames(symbol0_offset=...)``.
 """
 
-import ctypes
 from dataclasses import dataclass
 
 import numpy as np
