@@ -23,7 +23,12 @@
  *    (thread-local).
  *  - rx buffers must be 8-byte aligned and readable up to the next 16-byte
  *    boundary past the last sample used (TMA bulk copies move whole 16-byte
- *    granules; torch/cudaMalloc allocations satisfy this).
+ *    granules; torch/cudaMalloc allocations satisfy this).  Every entry that
+ *    reads a capture bounds-checks it against desc.rx_samples (ABI 2).
+ *  - Results never depend on the batch: a frame's bits, H, s_hat and weights
+ *    are bit-identical whatever n_frames (and whatever other frames) it is
+ *    launched with.  The antenna-sum order is a function of the frame shape
+ *    (N, M, D) only (ofdmrx_rx_plan reports it).
  */
 #ifndef OFDMRX_B200_H_
 #define OFDMRX_B200_H_
@@ -34,7 +39,7 @@
 extern "C" {
 #endif
 
-#define OFDMRX_ABI_VERSION 1
+#define OFDMRX_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define OFDMRX_API __attribute__((visibility("default")))
@@ -46,7 +51,7 @@ typedef enum {
   OFDMRX_OK = 0,
   OFDMRX_ERR_CONFIG = 1,   /* errors.ConfigurationError (errors.py:10-13) */
   OFDMRX_ERR_CONTRACT = 2, /* errors.ContractError (errors.py:28-31)      */
-  OFDMRX_ERR_INPUT = 3,    /* errors.FramingError / InputError (34-43)     */
+  OFDMRX_ERR_INPUT = 3,    /* errors.InputError (errors.py:40-43): capture too short, stream < PN */
   OFDMRX_ERR_NUMERIC = 4,  /* errors.NumericInputError (16-19)             */
   OFDMRX_ERR_CUDA = 5      /* device / launch failure                      */
 } ofdmrx_status;
@@ -77,14 +82,17 @@ typedef struct {
   int64_t frame_stride;   /* samples between frames                    */
   float eps;              /* MRC_WEIGHT_FLOOR (receiver.py:33) = 1e-12 */
   int32_t options;        /* OR of OFDMRX_OPT_* (0 = none)             */
+  int64_t rx_samples;     /* ABI 2: cf32 samples readable at rx; every sample a
+                           * call reads must lie below it (OFDMRX_ERR_INPUT
+                           * otherwise: extract_slots, receiver.py:278-283) */
 } ofdmrx_frame_desc;
 
 /* desc.options: the caller asserts every pilot value is exactly +1 or -1
  * (make_pilot's BPSK pilot, waveform.py:214-220); H = Y/P becomes a sign flip. */
 #define OFDMRX_OPT_PILOT_BPSK 1
-/* desc.options: never split a frame's antennas into on-device shards (one
- * CTA per frame even for small batches; results then do not depend on the
- * batch size). */
+/* desc.options: accepted for ABI-1 callers, no effect since ABI 2 (results
+ * never depend on the batch size; small batches spread each frame over a
+ * thread-block cluster instead of antenna shards). */
 #define OFDMRX_OPT_NO_SHARDS 2
 
 OFDMRX_API int ofdmrx_abi_version(void);
@@ -92,8 +100,31 @@ OFDMRX_API const char* ofdmrx_last_error(void);
 
 /* Host-only validation of a descriptor (no device access). Mirrors
  * OfdmConfig.__post_init__ (waveform.py:32-46) and extract_slots' bounds
- * check (receiver.py:278-283) against rx_len_samples (pass -1 to skip). */
-OFDMRX_API int ofdmrx_check_desc(const ofdmrx_frame_desc* desc, int64_t rx_len_samples);
+ * check (receiver.py:278-283) against desc.rx_samples. */
+OFDMRX_API int ofdmrx_check_desc(const ofdmrx_frame_desc* desc);
+
+/*
+ * Launch plan ofdmrx_rx_frames (mode 0) / ofdmrx_rx_partials (mode 1) would
+ * use for desc on the current device (needs a CUDA device).  `workers` fixes
+ * the arithmetic: the balanced kernel cuts a frame's data rows into `workers`
+ * contiguous ranges (antenna-sum order: ascending inside a range, ranges
+ * combined in order; den = per-worker strided partials combined in order);
+ * `cluster` / `ctas` only map those workers onto the GPU and change with
+ * n_frames.  The fused (lockstep) kernel sums antennas in ascending order.
+ */
+#define OFDMRX_KERNEL_BALANCED 1
+#define OFDMRX_KERNEL_FUSED 2
+typedef struct {
+  int32_t kernel;          /* OFDMRX_KERNEL_*                                  */
+  int32_t workers;         /* balanced: virtual FFT lanes per frame; fused: 0  */
+  int32_t lanes_per_cta;   /* FFT lanes per CTA                                */
+  int32_t cluster;         /* CTAs per frame (thread-block cluster size)       */
+  int32_t ctas;            /* grid size                                        */
+  int32_t threads;         /* threads per CTA                                  */
+  int32_t smem_bytes;      /* dynamic shared memory per CTA                    */
+  int32_t chunks;          /* fused: work items per frame (pilot recomputed)  */
+} ofdmrx_plan;
+OFDMRX_API int ofdmrx_rx_plan(const ofdmrx_frame_desc* desc, int32_t mode, int32_t zf, ofdmrx_plan* out);
 
 /*
  * Fused receive of F frames (one pass over HBM).  Replaces, per frame,
@@ -108,7 +139,7 @@ OFDMRX_API int ofdmrx_check_desc(const ofdmrx_frame_desc* desc, int64_t rx_len_s
  *   bits    [F,D*M*log2(Q)] u8 0/1, PipelineResult.bits order (required if D>0)
  *   zf      [F,D,N,M] cf32 per-antenna ZF output conj(H)Y/max(|H|^2,eps) (nullable)
  *   flags   [F] u32, OR-ed OFDMRX_FLAG_* (nullable; caller zeroes it)
- * MRC sums antennas in ascending order (mrc_seq, numba_backend.py:143-162).
+ * Antenna-sum order: see ofdmrx_rx_plan (a function of N, M, D only).
  */
 OFDMRX_API int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
                      float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream);
@@ -118,7 +149,7 @@ OFDMRX_API int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, c
  * detection (ofdmrx_detect outputs, no host round trip): symbol0 of frame f
  * = peak_index[f * peak_stride] + n_chips (DetectionResult.symbol0_offset,
  * sync.py:37-42, antenna 0).  desc.symbol0_offset must be 0; rows hold
- * n_samples samples.  Frames with peak_metric[f * peak_stride] < threshold
+ * n_samples samples (desc.rx_samples covers all F x N rows).  Frames with peak_metric[f * peak_stride] < threshold
  * get OFDMRX_FLAG_NOT_DETECTED, frames whose 1 + D symbols overrun the row get
  * OFDMRX_FLAG_OUT_OF_RANGE; both are skipped (their outputs unspecified).
  * flags is required.  This is the reference's detect_packet -> extract_slots

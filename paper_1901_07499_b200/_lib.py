@@ -11,15 +11,12 @@ from .errors import (
     ConfigurationError,
     ContractError,
     DeviceError,
-    FramingError,
+    InputError,
     NumericInputError,
 )
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libofdmrx_b200.so")
-# developer knob for A/B kernel experiments (scripts/fused_quick.py); the
-# product always loads the in-tree build
-LIB_PATH = os.environ.get("OFDMRX_LIB", LIB_PATH)
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, ERR_CONFIG, ERR_CONTRACT, ERR_INPUT, ERR_NUMERIC, ERR_CUDA = range(6)
 FLAG_NONFINITE = 1
@@ -32,7 +29,7 @@ OPT_NO_SHARDS = 2
 _STATUS_EXC = {
     ERR_CONFIG: ConfigurationError,
     ERR_CONTRACT: ContractError,
-    ERR_INPUT: FramingError,
+    ERR_INPUT: InputError,
     ERR_NUMERIC: NumericInputError,
     ERR_CUDA: DeviceError,
 }
@@ -53,7 +50,18 @@ class FrameDesc(ctypes.Structure):
         ("frame_stride", ctypes.c_int64),
         ("eps", ctypes.c_float),
         ("options", ctypes.c_int32),
+        ("rx_samples", ctypes.c_int64),
     ]
+
+
+class Plan(ctypes.Structure):
+    """ofdmrx_plan."""
+
+    _fields_ = [(name, ctypes.c_int32) for name in
+                ("kernel", "workers", "lanes_per_cta", "cluster", "ctas", "threads", "smem_bytes", "chunks")]
+
+
+KERNEL_BALANCED, KERNEL_FUSED = 1, 2
 
 
 _p = ctypes.c_void_p
@@ -88,7 +96,8 @@ _SDESC = ctypes.POINTER(SynthDesc)
 SIGNATURES = {
     "ofdmrx_abi_version": (ctypes.c_int, []),
     "ofdmrx_last_error": (ctypes.c_char_p, []),
-    "ofdmrx_check_desc": (ctypes.c_int, [_DESC, _i64]),
+    "ofdmrx_check_desc": (ctypes.c_int, [_DESC]),
+    "ofdmrx_rx_plan": (ctypes.c_int, [_DESC, _i32, _i32, ctypes.POINTER(Plan)]),
     "ofdmrx_rx_frames": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "ofdmrx_rx_partials": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _p, _p]),
     "ofdmrx_mrc_finish": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _f32, _p, _p, _p, _p, _p]),

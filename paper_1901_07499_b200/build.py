@@ -34,7 +34,7 @@ def _stale():
 
 def build_variant(name, defines, sources=None):
     """Experiment build: libofdmrx_b200_<name>.so under build/variants with
-    extra -D flags (A/B timing via OFDMRX_LIB=...; never the product)."""
+    extra -D flags (A/B timing via OFDMRX_VARIANT_LIB in scripts/fused_quick.py; never the product)."""
     outdir = os.path.join(HERE, "..", "build", "variants")
     os.makedirs(outdir, exist_ok=True)
     lib = os.path.abspath(os.path.join(outdir, f"libofdmrx_b200_{name}.so"))

@@ -56,7 +56,9 @@ int check_qam(int order) {
   return OFDMRX_OK;
 }
 
-int check_desc_impl(const ofdmrx_frame_desc* d, long long rx_len) {
+// rows_len: samples a row must hold (span of the 1 + D symbols, or the
+// detected-capture row length); the whole batch must lie inside rx_samples
+int check_desc_impl(const ofdmrx_frame_desc* d, long long rows_len = -1) {
   if (d == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
   if ((d->options & ~(OFDMRX_OPT_PILOT_BPSK | OFDMRX_OPT_NO_SHARDS)) != 0)
     return fail(OFDMRX_ERR_CONTRACT, "unknown descriptor options 0x%x", d->options);
@@ -74,12 +76,14 @@ int check_desc_impl(const ofdmrx_frame_desc* d, long long rx_len) {
   if (d->n_antennas > 1 && d->row_stride < span && d->row_stride != 0)
     return fail(OFDMRX_ERR_CONTRACT, "row_stride %lld shorter than the %lld samples a row needs",
                 (long long)d->row_stride, span);
-  if (rx_len >= 0 && d->n_frames > 0) {
+  if (d->rx_samples < 0) return fail(OFDMRX_ERR_CONTRACT, "rx_samples must be >= 0");
+  if (d->n_frames > 0) {
+    const long long row = rows_len >= 0 ? rows_len : span;
     const long long last = (long long)(d->n_frames - 1) * d->frame_stride +
-                           (long long)(d->n_antennas - 1) * d->row_stride + span;
-    if (last > rx_len)
-      return fail(OFDMRX_ERR_INPUT, "capture has %lld samples, %lld needed for %d symbols at offset %lld", rx_len,
-                  last, 1 + d->n_data, (long long)d->symbol0_offset);
+                           (long long)(d->n_antennas - 1) * d->row_stride + row;
+    if (last > d->rx_samples)
+      return fail(OFDMRX_ERR_INPUT, "capture has %lld samples, %lld needed for %d symbols at offset %lld",
+                  (long long)d->rx_samples, last, 1 + d->n_data, (long long)d->symbol0_offset);
   }
   return OFDMRX_OK;
 }
@@ -93,18 +97,6 @@ int check_align(const void* p, unsigned a, const char* what) {
   if ((reinterpret_cast<uintptr_t>(p) & (a - 1)) != 0)
     return fail(OFDMRX_ERR_CONTRACT, "%s must be %u-byte aligned", what, a);
   return OFDMRX_OK;
-}
-
-// Antenna shards per frame for a mode-0 launch: enough work items for ~3
-// waves of CTAs on the 148 SMs, keeping >= 16 antennas per shard and an
-// even split (power-of-two shards, so the finish tree over shards is the
-// reference ReductionPlan order, numerics.py:85-106).
-int pick_shards(const ofdmrx_frame_desc* d, const ofdmrx::FusedLaunch& l) {
-  const long long ctas = ((long long)d->n_frames * l.n_chunks + l.fpb - 1) / l.fpb;
-  int s = 1;
-  if (d->n_data == 0 || (d->options & OFDMRX_OPT_NO_SHARDS)) return 1;  // pilot-only frames: nothing to combine
-  while (ctas * s < 3 * 148 && d->n_antennas % (2 * s) == 0 && d->n_antennas / (2 * s) >= 16 && s < 64) s *= 2;
-  return s;
 }
 
 // stream-ordered scratch from the device's default pool, kept warm
@@ -147,10 +139,31 @@ struct Route {  // partial sums routed to the owners' peer inboxes
   int fpo, slot;
 };
 
+// Kernel choice and launch geometry for one fused call.  Everything that
+// fixes the arithmetic (balanced vs fused kernel, the balanced kernel's
+// worker count, the fused kernel's chunking) depends on the frame shape only;
+// n_frames only changes how the work is mapped onto CTAs.
+struct RxPlan {
+  bool balanced;
+  ofdmrx::BalancedPlan bp;
+  ofdmrx::FusedLaunch fl;
+};
+
+int make_plan(const ofdmrx_frame_desc* d, RxPlan* pl) {
+  *pl = RxPlan{};
+  pl->balanced = ofdmrx::balanced_plan(d->fft_len, d->n_antennas, d->n_data, d->n_frames,
+                                        ofdmrx::device_sm_count(), &pl->bp);
+  if (!pl->balanced) {
+    if (ofdmrx::fused_plan(d->fft_len, d->n_frames, d->n_data, &pl->fl) != cudaSuccess)
+      return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);
+  }
+  return OFDMRX_OK;
+}
+
 int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, int mode, void* H, void* s_hat,
                  float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream,
                  const Route* route = nullptr, const Detected* det = nullptr) {
-  if (int rc = check_desc_impl(d, -1)) return rc;
+  if (int rc = check_desc_impl(d, det != nullptr ? det->n_samples : -1)) return rc;
   if (d->n_frames == 0) return OFDMRX_OK;
   if (int rc = check_ptr(rx, "rx")) return rc;
   if (int rc = check_align(rx, 8, "rx")) return rc;
@@ -172,35 +185,26 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
       return fail(OFDMRX_ERR_CONTRACT, "n_frames %d is not a multiple of frames_per_owner %d", d->n_frames, route->fpo);
     if (route->slot < 0) return fail(OFDMRX_ERR_CONTRACT, "slot must be >= 0");
   }
-  ofdmrx::FusedLaunch l{};
-  cudaError_t e = ofdmrx::fused_plan(d->fft_len, d->n_frames, d->n_data, &l);
-  if (e != cudaSuccess) return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);
-  // Small batches of big frames (e.g. C4: 64 frames x 3 chunks on 148 SMs)
-  // leave SMs idle: split each frame's antennas into S shards on this device
-  // (partial MRC sums) and combine them with the pairwise-tree finish kernel.
-  const int shards = mode == 0 ? pick_shards(d, l) : 1;
-  if (shards > 1) {
-    if (e = ofdmrx::fused_plan(d->fft_len, d->n_frames * shards, d->n_data, &l); e != cudaSuccess)
-      return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);
-  }
+  RxPlan pl;
+  if (int rc = make_plan(d, &pl)) return rc;
   ofdmrx::FusedParams p{};
   p.rx = static_cast<const float2*>(rx);
   p.frame_stride = d->frame_stride;
   p.row_stride = d->row_stride;
   p.sym0 = d->symbol0_offset;
   p.n_frames = d->n_frames;
-  p.n_ant = d->n_antennas / shards;
+  p.n_ant = d->n_antennas;
   p.ant_total = d->n_antennas;
-  p.n_shards = shards;
+  p.n_shards = 1;
   p.cp = d->cp_len;
   p.n_data = d->n_data;
-  p.dc = l.dc;
-  p.n_chunks = l.n_chunks;
-  p.fpb = l.fpb;
-  p.n_work = d->n_frames * l.n_chunks * shards;
-  p.lanes = l.lanes;
-  p.ngroups = l.ngroups;
-  p.npilot = l.npilot;
+  p.dc = pl.fl.dc;
+  p.n_chunks = pl.fl.n_chunks;
+  p.fpb = pl.fl.fpb;
+  p.n_work = d->n_frames * pl.fl.n_chunks;
+  p.lanes = pl.fl.lanes;
+  p.ngroups = pl.fl.ngroups;
+  p.npilot = pl.fl.npilot;
   p.pilot = static_cast<const float2*>(pilot);
   p.eps = d->eps;
   qam_consts(d->qam_order, &p.qb, &p.levels, &p.qscale);
@@ -229,56 +233,21 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
     p.slot = route->slot;
   }
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (route == nullptr && ofdmrx::balanced_eligible(d->fft_len, d->n_antennas, d->n_data, mode, zf != nullptr, shards)) {
+  cudaError_t e;
+  if (pl.balanced) {
     void* hscratch = nullptr;
     if (p.H == nullptr) {  // H travels through L2 between the phases: scratch when the caller wants none
       if (int rc = scratch_alloc(&hscratch, (size_t)d->n_frames * d->n_antennas * d->fft_len * 8, st)) return rc;
       p.H = static_cast<float2*>(hscratch);
     }
-    e = ofdmrx::launch_balanced(p, st);
+    e = ofdmrx::launch_balanced(d->fft_len, p, pl.bp, st);
     cudaError_t e2 = hscratch != nullptr ? cudaFreeAsync(hscratch, st) : cudaSuccess;
     if (e != cudaSuccess) return cuda_fail(e, "rx_balanced_kernel launch");
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
     return OFDMRX_OK;
   }
-  if (shards == 1) {
-    e = ofdmrx::launch_fused(d->fft_len, p, l, st);
-    if (e != cudaSuccess) return cuda_fail(e, "rx_fused_kernel launch");
-    return OFDMRX_OK;
-  }
-  // sharded: partial sums into stream-ordered scratch, then finish
-  const size_t n_num = (size_t)shards * d->n_frames * d->n_data * d->fft_len;
-  const size_t n_den = (size_t)shards * d->n_frames * d->fft_len;
-  void* scratch = nullptr;
-  if (int rc = scratch_alloc(&scratch, n_num * 8 + n_den * 4, st)) return rc;
-  p.mode = 1;
-  p.s_hat = nullptr;
-  p.weights = nullptr;
-  p.bits = nullptr;
-  p.part_num = static_cast<float2*>(scratch);
-  p.part_den = reinterpret_cast<float*>(static_cast<char*>(scratch) + n_num * 8);
-  e = ofdmrx::launch_fused(d->fft_len, p, l, st);
-  if (e == cudaSuccess && d->n_data > 0) {
-    ofdmrx::FinishParams fp{};
-    fp.num = p.part_num;
-    fp.den = p.part_den;
-    fp.parts = shards;
-    fp.n_frames = d->n_frames;
-    fp.n_data = d->n_data;
-    fp.M = d->fft_len;
-    fp.eps = d->eps;
-    fp.qb = p.qb;
-    fp.levels = p.levels;
-    fp.qscale = p.qscale;
-    fp.s_hat = static_cast<float2*>(s_hat);
-    fp.weights = weights;
-    fp.bits = bits;
-    fp.flags = flags;
-    e = ofdmrx::launch_finish(fp, st);
-  }
-  cudaError_t e2 = cudaFreeAsync(scratch, st);
-  if (e != cudaSuccess) return cuda_fail(e, "sharded rx_fused_kernel / finish_kernel launch");
-  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
+  e = ofdmrx::launch_fused(d->fft_len, p, pl.fl, st);
+  if (e != cudaSuccess) return cuda_fail(e, "rx_fused_kernel launch");
   return OFDMRX_OK;
 }
 
@@ -315,6 +284,19 @@ int sync_common(const void* rx, int32_t n_frames, int32_t n_antennas, int64_t n_
 }
 
 }  // namespace
+
+namespace ofdmrx {
+int device_sm_count() {
+  static int counts[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  if (dev < 64 && counts[dev] > 0) return counts[dev];
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  if (dev < 64) counts[dev] = n;
+  return n;
+}
+}  // namespace ofdmrx
 
 extern "C" {
 
@@ -374,8 +356,36 @@ int ofdmrx_abi_version(void) { return OFDMRX_ABI_VERSION; }
 
 const char* ofdmrx_last_error(void) { return g_last_error.c_str(); }
 
-int ofdmrx_check_desc(const ofdmrx_frame_desc* desc, int64_t rx_len_samples) {
-  return check_desc_impl(desc, rx_len_samples);
+int ofdmrx_check_desc(const ofdmrx_frame_desc* desc) { return check_desc_impl(desc); }
+
+int ofdmrx_rx_plan(const ofdmrx_frame_desc* desc, int32_t mode, int32_t zf, ofdmrx_plan* out) {
+  if (int rc = check_desc_impl(desc)) return rc;
+  if (int rc = check_ptr(out, "out")) return rc;
+  if (mode != 0 && mode != 1) return fail(OFDMRX_ERR_CONTRACT, "mode must be 0 or 1");
+  (void)zf;  // the ZF output changes neither the kernel nor the order
+  RxPlan pl;
+  if (int rc = make_plan(desc, &pl)) return rc;
+  *out = ofdmrx_plan{};
+  if (pl.balanced) {
+    out->kernel = OFDMRX_KERNEL_BALANCED;
+    out->workers = pl.bp.workers;
+    out->lanes_per_cta = pl.bp.lanes_per_cta;
+    out->cluster = pl.bp.cluster;
+    out->ctas = desc->n_frames * pl.bp.cluster;
+    out->threads = pl.bp.lanes_per_cta * pl.bp.fft_lane_threads;
+    out->smem_bytes = (int32_t)ofdmrx::balanced_smem_bytes(desc->fft_len, pl.bp.lanes_per_cta);
+    out->chunks = 1;
+  } else {
+    out->kernel = OFDMRX_KERNEL_FUSED;
+    out->workers = 0;
+    out->lanes_per_cta = pl.fl.lanes;
+    out->cluster = 1;
+    out->ctas = pl.fl.grid;
+    out->threads = pl.fl.threads;
+    out->smem_bytes = (int32_t)pl.fl.smem;
+    out->chunks = pl.fl.n_chunks;
+  }
+  return OFDMRX_OK;
 }
 
 int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
@@ -498,7 +508,7 @@ int ofdmrx_mrc_finish(int32_t n_frames, int32_t n_data, int32_t fft_len, int32_t
 
 int ofdmrx_fft_shift(const ofdmrx_frame_desc* desc, int32_t first_symbol, int32_t n_symbols, const void* rx, void* Y,
                      void* stream) {
-  if (int rc = check_desc_impl(desc, -1)) return rc;
+  if (int rc = check_desc_impl(desc)) return rc;
   if (first_symbol < 0 || n_symbols < 0 || first_symbol + n_symbols > 1 + desc->n_data)
     return fail(OFDMRX_ERR_CONTRACT, "symbol range [%d, %d) outside the frame's %d symbols", first_symbol,
                 first_symbol + n_symbols, 1 + desc->n_data);
@@ -566,7 +576,7 @@ int ofdmrx_mrc(int32_t n_frames, int32_t n_data, int32_t n_antennas, int32_t fft
 }
 
 int ofdmrx_stage_symbols(const ofdmrx_frame_desc* desc, const void* src, void* dst, void* stream) {
-  if (int rc = check_desc_impl(desc, -1)) return rc;
+  if (int rc = check_desc_impl(desc)) return rc;
   const long long F = desc->n_frames, N = desc->n_antennas, S = 1 + desc->n_data, M = desc->fft_len;
   if (F == 0) return OFDMRX_OK;
   if (int rc = check_ptr(src, "src")) return rc;

@@ -80,11 +80,22 @@ struct FusedLaunch {
   size_t smem;
 };
 
-// Balanced M = 1024 variant (rx_balanced.cu): pilot rows first, data rows split
-// evenly over the warps, H through L2.  Needs p.H (caller supplies scratch).
-bool balanced_eligible(int M, int n_ant, int n_data, int mode, bool zf, int shards);
-size_t balanced_smem_bytes();
-cudaError_t launch_balanced(const FusedParams& p, cudaStream_t s);
+// Balanced variant (rx_balanced.cu), M in {1024, 2048, 4096}: V virtual FFT
+// lanes per frame (fixed by the frame shape: the antenna-sum order), mapped
+// onto `cluster` CTAs of `lanes_per_cta` lanes each (chosen per batch).
+// Needs p.H (caller supplies scratch).
+struct BalancedPlan {
+  int workers;          // V virtual lanes per frame
+  int lanes_per_cta;    // LPC
+  int cluster;          // CTAs per frame (thread-block cluster size)
+  int fft_lane_threads; // G
+};
+bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out);
+size_t balanced_smem_bytes(int M, int lanes_per_cta);
+cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp, cudaStream_t s);
+
+// multiprocessor count of the current device (cached per device)
+int device_sm_count();
 
 // returns cudaErrorInvalidValue for unsupported M
 cudaError_t fused_plan(int M, int n_frames, int n_data, FusedLaunch* out);

@@ -1,28 +1,33 @@
-// Balanced fused receive for M = 1024 (one 32-thread FFT lane per warp),
-// D <= 12 data symbols: the same stages as rx_fused_kernel (CP drop + FFT +
-// fftshift -> LS -> MRC -> divide -> demap, receiver.py:238-267,308-348) with
-// a different work split.
+// Balanced fused receive for M in {1024, 2048, 4096} (FFT lanes of G = 32,
+// 64, 128 threads, P = 32 points per thread): CP drop + FFT + fftshift -> LS
+// -> MRC -> divide -> demap (receiver.py:238-267,308-348) with the work of a
+// frame cut into V "virtual lanes" whose arithmetic does not depend on how
+// the lanes are mapped onto CTAs.
 //
-// rx_fused_kernel gives each warp one OFDM symbol for all N antennas, so the
-// data warps walk the antennas in lockstep behind the pilot units' H ring and
-// every scheduler carries whole symbols: with 1 + 10 symbols on 12 warps, two
-// schedulers run three full data warps while the other two carry half-busy
-// pilot warps (profiles/experiments_r01_C3.md).  Here:
-//   phase A  every warp FFTs pilot rows n = w, w + 12, ...: H_n = Y_n conj(P)
-//            is written to the H output (global, L2-resident), |H_n|^2 is
-//            accumulated into a per-warp den partial;
-//   barrier  (+ generic -> async proxy fence for the H stores)
+// Per frame (V fixed by the frame shape, never by the batch size):
+//   phase A  lane v FFTs pilot rows n = v, v + V, ...: H_n = Y_n conj(P) is
+//            written to the H output (global, L2-resident), |H_n|^2 is
+//            accumulated into the lane's den partial (TMEM);
+//            cluster barrier ARRIVE (release: H rows published)
 //   phase B  the D x N data rows, symbol-major (antennas ascending inside a
-//            symbol), are cut into 12 equal contiguous ranges.  A warp walks
-//            its range with the rx row of step k+1 TMA-prefetched; after the
-//            FFT's last pass has read the slot, H_n is TMA-loaded from L2 into
-//            that slot for the MAC.  Accumulators (<= 2 symbols per warp: its
-//            range is at most N rows) live in TMEM.  No warp waits for another
-//            inside the loop.
-//   epilogue the owner of each symbol (the warp holding its first row) adds
-//            the partial of the warps continuing it (fixed order), den is the
-//            fixed-order sum of the 12 warp partials; divide, demap, store.
-// Every scheduler gets 3 warps x (704 / 12) rows of the same mix of work.
+//            symbol), are cut into V equal contiguous ranges (<= N rows each,
+//            so a lane touches at most 2 symbols).  A lane streams its range:
+//            the next rx row is TMA-prefetched, and once the FFT's last pass
+//            has its inputs the lane loads H_n from L2 into registers
+//            (ld.global.cg) so the latency hides under that pass.  The first
+//            of these loads is preceded by the cluster barrier WAIT (acquire),
+//            so a lane that finished its pilot rows early runs its first data
+//            FFT instead of idling.  MRC accumulators (<= 2 symbols) in TMEM.
+//   epilogue den = sum of the V lane partials in lane order; the owner of
+//            each symbol (the lane holding its first row) adds the partials
+//            of the lanes continuing it, in lane order, then divides, demaps
+//            and stores (mode 0) or stores the un-normalised sums (mode 1).
+//
+// Mapping: a CTA runs LPC lanes; a thread-block cluster of CL = V / LPC CTAs
+// runs one frame.  Partials of lanes in other CTAs of the cluster are read
+// through distributed shared memory (mapa + ld.shared::cluster), so a small
+// batch spreads each frame over several SMs with results bit-identical to
+// the one-CTA-per-frame launch a large batch uses.
 #include "ofdmrx_fft.cuh"
 #include "ofdmrx_internal.h"
 
@@ -30,175 +35,201 @@ namespace ofdmrx {
 
 namespace {
 
-constexpr int BW = 12;     // warps = FFT lanes per CTA
-constexpr int BM = 1024;
-using BPI = PlanInfo<BM>;
-constexpr int BP = BPI::P;  // 32 points per thread
-constexpr int BSS = BPI::SLOT;
-constexpr int BACC = 2 * BP;             // floats per accumulator set
-constexpr int BCOLS = 2 * BACC + BP;     // 2 sets + den partial
-constexpr size_t BBAR = 512;             // mbarriers + TMEM address word
+constexpr int BMAXW = 12;       // warps per CTA at most (register budget 168 x 384)
+constexpr size_t BBAR = 512;    // mbarriers + TMEM address word
+constexpr int BMAX_CLUSTER = 8; // portable cluster size
 
-__device__ __forceinline__ int range_lo(int w, int total) { return (int)((long long)total * w / BW); }
+template <int M>
+struct BalCfg {
+  using PI = PlanInfo<M>;
+  static constexpr int P = PI::P, G = PI::G, LW = G / 32, SLOT = PI::SLOT;
+  static constexpr int ACC = 2 * P;             // floats per accumulator set
+  static constexpr int COLS = 2 * ACC + P;      // 2 sets + den partial, per warp
+  static constexpr int LPC_MAX = BMAXW / LW;    // lanes per CTA at most
+  static_assert(P == 32 && G >= 32, "balanced kernel: 32 points per thread, whole-warp lanes");
+  static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * SLOT * sizeof(float2); }
+};
 
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
+__device__ __forceinline__ int range_lo(int v, int total, int V) { return (int)((long long)total * v / V); }
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+// split cluster barrier: every thread of every CTA of the cluster arrives
+// once, then waits once (release / acquire at cluster scope)
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 ld_dsmem2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
 }
 
-template <bool BPSK>
-__global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedParams p) {
+template <int M, bool BPSK, bool ZF>
+__global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedParams p) {
+  using BC = BalCfg<M>;
+  constexpr int P = BC::P, G = BC::G, LW = BC::LW, SS = BC::SLOT, ACC = BC::ACC, COLS = BC::COLS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
-  const int f = blockIdx.x;
+  const int lpc = blockDim.x / G;
+  const int l = threadIdx.x / G, t = threadIdx.x % G, w = threadIdx.x >> 5;
+  const uint32_t crank = cluster_ctarank();
+  const int V = lpc * (int)cluster_nctarank();
+  const int v = (int)crank * lpc + l;  // virtual lane of this thread
+  const int f = (int)cluster_id_x();   // one cluster per frame
   const int N = p.n_ant, D = p.n_data;
   uint32_t reject = 0u;
-  const long long sym0 = frame_sym0(p, f, BM, &reject);
-  if (reject != 0u) {  // not detected / out of range: flagged, no traffic, no outputs
-    if (threadIdx.x == 0 && p.flags != nullptr) atomicOr(&p.flags[f], reject);
+  const long long sym0 = frame_sym0(p, f, M, &reject);
+  if (reject != 0u) {  // not detected / out of range: the whole cluster leaves; flagged, no traffic
+    if (threadIdx.x == 0 && crank == 0 && p.flags != nullptr) atomicOr(&p.flags[f], reject);
     return;
   }
-  uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [BW][2]
-  uint64_t* h_bar = rx_bar + 2 * BW;                          // [BW]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_bar + BW);
-  float2* slot_base = reinterpret_cast<float2*>(smem_raw + BBAR) + (size_t)w * 2 * BSS;
+  uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [lpc][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rx_bar + 2 * BC::LPC_MAX);
+  float2* slot_base = reinterpret_cast<float2*>(smem_raw + BBAR) + (size_t)l * 2 * SS;
   const bool leader = t == 0;
+  auto lane_sync = [&]() {
+    if constexpr (LW == 1) __syncwarp();
+    else named_bar_sync(1 + l, G);
+  };
 
-  if (threadIdx.x < 3 * BW) mbar_init(&rx_bar[threadIdx.x], 1);
+  if (threadIdx.x < 2 * lpc) mbar_init(&rx_bar[threadIdx.x], 1);
   fence_mbar_init();
-  if (w == 0) tmem_alloc(tmem_slot, 512);
+  const int nw = lpc * LW;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(((nw + 3) / 4) * COLS)) cols <<= 1;
+  if (w == 0) tmem_alloc(tmem_slot, cols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tbase = *tmem_slot + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * BCOLS);
-  const uint32_t t_den = tbase + 2 * BACC;
+  const uint32_t tbase = *tmem_slot + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * COLS);
+  const uint32_t t_den = tbase + 2 * ACC;
 
   const float2* frame = p.rx + (long long)f * p.frame_stride + sym0 + p.cp;
-  float2* Hf = p.H + (long long)f * N * BM;
-  // rx row (symbol s, antenna n): TMA into stage st of this warp
-  auto row_addr = [&](int s, int n) { return frame + (long long)n * p.row_stride + (long long)s * (BM + p.cp); };
+  float2* Hf = p.H + (long long)f * N * M;
+  auto row_addr = [&](int s, int n) { return frame + (long long)n * p.row_stride + (long long)s * (M + p.cp); };
   auto issue_rx = [&](const float2* src, int st) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(src);
     const uintptr_t start = a & ~uintptr_t(15);
-    const uint32_t bytes = (uint32_t)(((a + (uintptr_t)BM * 8u + 15u) & ~uintptr_t(15)) - start);
-    uint64_t* bar = &rx_bar[2 * w + st];
+    const uint32_t bytes = (uint32_t)(((a + (uintptr_t)M * 8u + 15u) & ~uintptr_t(15)) - start);
+    uint64_t* bar = &rx_bar[2 * l + st];
     mbar_arrive_expect_tx(bar, bytes);
-    // policy made at the issue (1 instruction) rather than held in 2 registers
-    tma_bulk_g2s(slot_base + (size_t)st * BSS, reinterpret_cast<const void*>(start), bytes, bar,
+    tma_bulk_g2s(slot_base + (size_t)st * SS, reinterpret_cast<const void*>(start), bytes, bar,
                  l2_evict_first_policy());
   };
-#ifdef OFDMRX_BAL_H_TMA
-  uint32_t h_phase = 0u;
-#endif
   // stage st = k & 1 is used at every other step, so its phase is (k >> 1) & 1
-  // (a per-stage phase array indexed by st would live in local memory)
-  auto wait_rx = [&](int kk) { mbar_wait_parity(&rx_bar[2 * w + (kk & 1)], (uint32_t)(kk >> 1) & 1u); };
+  auto wait_rx = [&](int kk) { mbar_wait_parity(&rx_bar[2 * l + (kk & 1)], (uint32_t)(kk >> 1) & 1u); };
 
   // ---------------- phase A: pilot rows --------------------------------------
   uint32_t pmask = 0;
   if constexpr (BPSK) {
 #pragma unroll
-    for (int i = 0; i < BP; ++i) pmask |= (__ldg(p.pilot + shifted_bin<BM>(i, t)).x < 0.0f ? 1u : 0u) << i;
+    for (int i = 0; i < P; ++i) pmask |= (__ldg(p.pilot + shifted_bin<M>(i, t)).x < 0.0f ? 1u : 0u) << i;
   }
   {  // zero the den partial and both accumulator sets (TMEM)
-    float z[BACC];
+    float z[ACC];
 #pragma unroll
-    for (int i = 0; i < BACC; ++i) z[i] = 0.0f;
-    tmem_st<BP>(t_den, z);
-    tmem_st<BACC>(tbase, z);
-    tmem_st<BACC>(tbase + BACC, z);
+    for (int i = 0; i < ACC; ++i) z[i] = 0.0f;
+    tmem_st<P>(t_den, z);
+    tmem_st<ACC>(tbase, z);
+    tmem_st<ACC>(tbase + ACC, z);
   }
   const int total = D * N;
-  const int r0 = range_lo(w, total), r1 = range_lo(w + 1, total);
+  const int r0 = range_lo(v, total, V), r1 = range_lo(v + 1, total, V);
   int k = 0;  // stage counter across both phases
-  if (leader && w < N) issue_rx(row_addr(0, w), 0);
-  float2 v[BP];
-  for (int n = w; n < N; n += BW, ++k) {
+  if (leader && v < N) issue_rx(row_addr(0, v), 0);
+  float2 y[P];
+  for (int n = v; n < N; n += V, ++k) {
     const int st = k & 1;
-    float2* slot = slot_base + (size_t)st * BSS;
+    float2* slot = slot_base + (size_t)st * SS;
     if (leader) {
-      if (n + BW < N) issue_rx(row_addr(0, n + BW), st ^ 1);
+      if (n + V < N) issue_rx(row_addr(0, n + V), st ^ 1);
       else if (r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), st ^ 1);  // first data row of phase B
     }
     wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(0, n)) >> 3) & 1);
     const float2* src = slot + sh;
-    fft_forward<BM>(v, slot, t, [&](int idx) { return src[idx]; }, [] { __syncwarp(); });
+    fft_forward<M>(y, slot, t, [&](int idx) { return src[idx]; }, lane_sync);
     fence_proxy_async_smem();
-    __syncwarp();
-    float2* hdst = Hf + (long long)n * BM + t;
-    float dp[BP];
+    lane_sync();
+    float2* hdst = Hf + (long long)n * M + t;
+    float dp[P];
     tmem_wait_st();
-    tmem_ld<BP>(t_den, dp);
+    tmem_ld<P>(t_den, dp);
     tmem_wait_ld();
 #pragma unroll
-    for (int i = 0; i < BP; ++i) {
-      const float2 y = v[i];
+    for (int i = 0; i < P; ++i) {
+      const float2 yy = y[i];
       float2 h;
       if constexpr (BPSK) {
         const uint32_t sgn = (pmask << (31 - i)) & 0x80000000u;
-        h = make_float2(__uint_as_float(__float_as_uint(y.x) ^ sgn), __uint_as_float(__float_as_uint(y.y) ^ sgn));
+        h = make_float2(__uint_as_float(__float_as_uint(yy.x) ^ sgn), __uint_as_float(__float_as_uint(yy.y) ^ sgn));
       } else {
-        const float2 pc = __ldg(p.pilot + shifted_bin<BM>(i, t));
-        h = make_float2(fmaf(y.y, pc.y, y.x * pc.x), fmaf(-y.x, pc.y, y.y * pc.x));
+        const float2 pc = __ldg(p.pilot + shifted_bin<M>(i, t));
+        h = make_float2(fmaf(yy.y, pc.y, yy.x * pc.x), fmaf(-yy.x, pc.y, yy.y * pc.x));
       }
       dp[i] = fmaf(h.x, h.x, fmaf(h.y, h.y, dp[i]));
-      hdst[shifted_bin<BM>(i, 0)] = h;
+      hdst[shifted_bin<M>(i, 0)] = h;
     }
-    tmem_st<BP>(t_den, dp);
+    tmem_st<P>(t_den, dp);
   }
-  if (leader && w >= N && r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), k & 1);  // no pilot rows
+  if (leader && v >= N && r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), k & 1);  // no pilot rows
   tmem_wait_st();
-  // H rows (generic stores of all warps) -> phase B loads (the TMA variant
-  // also needs the generic -> async proxy fences).  A per-antenna mbarrier
-  // instead of this barrier measured 0.4 % slower.
-  fence_proxy_async_global();
-  __syncthreads();
-  fence_proxy_async_global();
+  // H rows of this lane are published; lanes of the cluster acquire them
+  // before their first H load (wait inside the first data FFT, below)
+  cluster_arrive();
+  bool h_acquired = false;
 
-  // ---------------- phase B: this warp's data rows -----------------------
+  // ---------------- phase B: this lane's data rows -------------------------
   const int d_first = r0 < r1 ? r0 / N : 0;
-  int d = d_first, n = r0 - d_first * N;   // current row (symbol-major)
-  int dn = d, nn = n + 1;                  // next row
+  int d = d_first, n = r0 - d_first * N;  // current row (symbol-major)
+  int dn = d, nn = n + 1;                 // next row
   if (nn == N) nn = 0, ++dn;
   for (int r = r0; r < r1; ++r, ++k) {
     const int st = k & 1;
-    float2* slot = slot_base + (size_t)st * BSS;
+    float2* slot = slot_base + (size_t)st * SS;
     if (leader && r + 1 < r1) issue_rx(row_addr(1 + dn, nn), st ^ 1);
     wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(1 + d, n)) >> 3) & 1);
     const float2* src = slot + sh;
-#ifdef OFDMRX_BAL_H_TMA
-    fft_forward<BM>(v, slot, t, [&](int idx) { return src[idx]; }, [] { __syncwarp(); },
-                    [&] {  // slot consumed: bring H_n from L2 into it while the last pass runs
-                      fence_proxy_async_smem();
-                      __syncwarp();
-                      if (leader) {
-                        mbar_arrive_expect_tx(&h_bar[w], BM * 8u);
-                        tma_bulk_g2s(slot, Hf + (long long)n * BM, BM * 8u, &h_bar[w], l2_evict_first_policy());
-                      }
-                    });
-    const uint32_t tacc = tbase + (uint32_t)((d - d_first) * BACC);
-    float a[BACC];
-    tmem_wait_st();
-    tmem_ld<BACC>(tacc, a);
-    tmem_wait_ld();
-    mbar_wait_parity(&h_bar[w], h_phase);
-    h_phase ^= 1u;
-    auto h_at = [&](int i) { return slot[shifted_bin<BM>(i, t)]; };
-#else
     // H_n straight from L2 into registers (ld.global.cg: coherent with the
-    // phase-A stores of the other warps), issued once the last FFT pass has
+    // phase-A stores of the other lanes), issued once the last FFT pass has
     // its inputs so the latency hides under that pass's butterflies
-    float2 hreg[BP];
-    const float2* hsrc = Hf + (long long)n * BM + t;
-    fft_forward<BM>(v, slot, t, [&](int idx) { return src[idx]; }, [] { __syncwarp(); }, [&] {
+    float2 hreg[P];
+    const float2* hsrc = Hf + (long long)n * M + t;
+    fft_forward<M>(y, slot, t, [&](int idx) { return src[idx]; }, lane_sync, [&] {
+      if (!h_acquired) {
+        cluster_wait();
+        h_acquired = true;
+      }
 #pragma unroll
-      for (int i = 0; i < BP; ++i) hreg[i] = __ldcg(hsrc + shifted_bin<BM>(i, 0));
+      for (int i = 0; i < P; ++i) hreg[i] = __ldcg(hsrc + shifted_bin<M>(i, 0));
     });
-    const uint32_t tacc = tbase + (uint32_t)((d - d_first) * BACC);
+    const uint32_t tacc = tbase + (uint32_t)((d - d_first) * ACC);
     tmem_wait_st();
-    // MAC in 16-column TMEM chunks: keeps v + hreg + one chunk in registers
-    static_for<BACC / 16>([&](auto ci) {
+    // MAC in 16-column TMEM chunks: keeps y + hreg + one chunk in registers
+    static_for<ACC / 16>([&](auto ci) {
       constexpr int c = decltype(ci)::value;
       float a[16];
       tmem_ld16(tacc + 16 * c, a);
@@ -207,136 +238,264 @@ __global__ void __launch_bounds__(BW * 32, 1) rx_balanced_kernel(const FusedPara
       for (int q = 0; q < 8; ++q) {
         const int i = 8 * c + q;
         const float2 h = hreg[i];
-        const float2 y = v[i];
+        const float2 yy = y[i];
         // conj(H) * Y = h.x * (y.x, y.y) + h.y * (y.y, -y.x)  (numba_backend.py:149-150)
-        const float2 m = upk(fma2(bc(h.y), pk(y.y, -y.x), fma2(bc(h.x), pk(y), pk(a[2 * q], a[2 * q + 1]))));
+        const float2 m = upk(fma2(bc(h.y), pk(yy.y, -yy.x), fma2(bc(h.x), pk(yy), pk(a[2 * q], a[2 * q + 1]))));
         a[2 * q] = m.x;
         a[2 * q + 1] = m.y;
       }
       tmem_st16(tacc + 16 * c, a);
     });
-#endif
-#ifdef OFDMRX_BAL_H_TMA
+    if constexpr (ZF) {  // per-antenna ZF output conj(H) Y / max(|H|^2, eps) (1-row mrc_combine)
+      float2* zdst = p.zf + (((long long)f * D + d) * N + n) * M + t;
 #pragma unroll
-    for (int i = 0; i < BP; ++i) {
-      const float2 h = h_at(i);
-      const float2 y = v[i];
-      const float2 m = upk(fma2(bc(h.y), pk(y.y, -y.x), fma2(bc(h.x), pk(y), pk(a[2 * i], a[2 * i + 1]))));
-      a[2 * i] = m.x;
-      a[2 * i + 1] = m.y;
+      for (int i = 0; i < P; ++i) {
+        const float2 h = hreg[i], yy = y[i];
+        const float dd = fmaxf(fmaf(h.x, h.x, h.y * h.y), p.eps);
+        zdst[shifted_bin<M>(i, 0)] = make_float2(fmaf(h.x, yy.x, h.y * yy.y) / dd, fmaf(h.x, yy.y, -h.y * yy.x) / dd);
+      }
     }
-    tmem_st<BACC>(tacc, a);
-#endif
     fence_proxy_async_smem();  // reads of this slot before its next TMA refill
-    __syncwarp();
+    lane_sync();
     d = dn, n = nn;
     if (++nn == N) nn = 0, ++dn;
   }
+  if (!h_acquired) cluster_wait();
 
   // ---------------- epilogue -------------------------------------------------
+  // every lane parks its den partial (and the partial of a symbol it
+  // continues) in the now idle TMA slots of its CTA; the cluster reads them
   tmem_wait_st();
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  float* denbuf = reinterpret_cast<float*>(smem_raw + BBAR);                       // [BW][BM]
-  float2* partbuf = reinterpret_cast<float2*>(smem_raw + BBAR + (size_t)BW * BM * 4);  // [BW][BM]
+  float* denbuf = reinterpret_cast<float*>(smem_raw + BBAR);                          // [lpc][M]
+  float2* partbuf = reinterpret_cast<float2*>(smem_raw + BBAR + (size_t)lpc * M * 4);  // [lpc][M]
   const bool has_rows = r0 < r1;
-  const bool continues = has_rows && (r0 % N) != 0;  // set 0 continues a symbol owned by an earlier warp
+  const bool continues = has_rows && (r0 % N) != 0;  // set 0 continues a symbol owned by an earlier lane
   {
-    float dp[BP];
-    tmem_ld<BP>(t_den, dp);
+    float dp[P];
+    tmem_ld<P>(t_den, dp);
     tmem_wait_ld();
 #pragma unroll
-    for (int i = 0; i < BP; ++i) denbuf[w * BM + i * 32 + t] = dp[i];
+    for (int i = 0; i < P; ++i) denbuf[l * M + i * G + t] = dp[i];
     if (continues) {
-      float a[BACC];
-      tmem_ld<BACC>(tbase, a);
+      float a[ACC];
+      tmem_ld<ACC>(tbase, a);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < BP; ++i) partbuf[w * BM + i * 32 + t] = make_float2(a[2 * i], a[2 * i + 1]);
+      for (int i = 0; i < P; ++i) partbuf[l * M + i * G + t] = make_float2(a[2 * i], a[2 * i + 1]);
     }
   }
-  __syncthreads();
-  uint32_t flag = 0;
-  float den[BP];
-#pragma unroll
-  for (int i = 0; i < BP; ++i) {
-    float s = 0.0f;
-    for (int q = 0; q < BW; ++q) s += denbuf[q * BM + i * 32 + t];
-    den[i] = s;
-  }
-  if (w == 0) {
-    if (p.weights != nullptr) {
-      float* wd = p.weights + (long long)f * BM + t;
-#pragma unroll
-      for (int i = 0; i < BP; ++i) wd[shifted_bin<BM>(i, 0)] = den[i];
-    }
-#pragma unroll
-    for (int i = 0; i < BP; ++i) {
-      if (!isfinite(den[i])) flag |= 1u;
-      if (den[i] < p.eps) flag |= 2u;
-    }
-  }
-  // the symbol owned by this warp: its first row lies in [r0, r1)
+  cluster_arrive();
+  cluster_wait();
+
+  // the symbol owned by this lane: its first row lies in [r0, r1)
   const int d_own = has_rows ? (r0 + N - 1) / N : D;
-  if (has_rows && d_own * N < r1 && d_own < D) {
-    float a[BACC];
-    tmem_ld<BACC>(tbase + (uint32_t)((d_own - d_first) * BACC), a);
-    tmem_wait_ld();
-    // add the partials of the following warps that continue this symbol
-    for (int q = w + 1; q < BW; ++q) {
-      const int q0 = range_lo(q, total), q1 = range_lo(q + 1, total);
-      if (q0 >= q1 || q0 / N != d_own || q0 % N == 0) break;
+  const bool owns = has_rows && d_own < D && d_own * N < r1;
+  uint32_t flag = 0;
+  if (owns || v == 0) {
+    // den = fixed-order sum of the V lane partials (lane q lives in CTA q / lpc)
+    float den[P];
 #pragma unroll
-      for (int i = 0; i < BP; ++i) {
-        const float2 pv = partbuf[q * BM + i * 32 + t];
-        a[2 * i] += pv.x;
-        a[2 * i + 1] += pv.y;
+    for (int i = 0; i < P; ++i) den[i] = 0.0f;
+    for (int q = 0; q < V; ++q) {
+      const uint32_t rk = (uint32_t)(q / lpc);
+      const float* src = denbuf + (q - (int)rk * lpc) * M + t;
+      if (rk == crank) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) den[i] += src[i * G];
+      } else {
+        const uint32_t ra = dsmem_addr(src, rk);
+#pragma unroll
+        for (int i = 0; i < P; ++i) den[i] += ld_dsmem(ra + 4u * (uint32_t)(i * G));
       }
     }
-    const QamParams qp{p.qb, p.levels, p.qscale};
-    const long long sym_base = ((long long)f * D + d_own) * BM;
-    float2* sdst = p.s_hat + sym_base + t;
-    uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
+    if (v == 0) {
+      float* wdst = p.mode == 0 ? p.weights : p.part_den;
+      long long wrow = f;
+      if (p.mode == 1 && p.den_dst != nullptr) {  // routed to the frame's owner (peer exchange)
+        const int o = f / p.fpo;
+        wdst = p.den_dst[o];
+        wrow = (long long)p.slot * p.fpo + (f - o * p.fpo);
+      }
+      if (wdst != nullptr) {
+        float* wd = wdst + wrow * M + t;
 #pragma unroll
-    for (int i = 0; i < BP; ++i) {
-      const float dd = fmaxf(den[i], p.eps);
-      const float2 shv = make_float2(a[2 * i] / dd, a[2 * i + 1] / dd);
-      if (!isfinite(shv.x) || !isfinite(shv.y)) flag |= 1u;
-      const int j = shifted_bin<BM>(i, 0);
-      sdst[j] = shv;
-      demap_store(shv, qp, bdst + (long long)j * p.qb);
+        for (int i = 0; i < P; ++i) wd[shifted_bin<M>(i, 0)] = den[i];
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        if (!isfinite(den[i])) flag |= 1u;
+        if (p.mode == 0 && den[i] < p.eps) flag |= 2u;  // partial sums: erasure is decided after the combine
+      }
+    }
+    if (owns) {
+      float a[ACC];
+      tmem_ld<ACC>(tbase + (uint32_t)((d_own - d_first) * ACC), a);
+      tmem_wait_ld();
+      // add the partials of the following lanes that continue this symbol, in
+      // lane order; lanes without rows are skipped (N < V leaves some empty)
+      for (int q = v + 1; q < V; ++q) {
+        const int q0 = range_lo(q, total, V), q1 = range_lo(q + 1, total, V);
+        if (q0 >= q1) continue;
+        if (q0 / N != d_own || q0 % N == 0) break;
+        const uint32_t rk = (uint32_t)(q / lpc);
+        const float2* src = partbuf + (q - (int)rk * lpc) * M + t;
+        if (rk == crank) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const float2 pv = src[i * G];
+            a[2 * i] += pv.x;
+            a[2 * i + 1] += pv.y;
+          }
+        } else {
+          const uint32_t ra = dsmem_addr(src, rk);
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const float2 pv = ld_dsmem2(ra + 8u * (uint32_t)(i * G));
+            a[2 * i] += pv.x;
+            a[2 * i + 1] += pv.y;
+          }
+        }
+      }
+      const long long sym_base = ((long long)f * D + d_own) * M;
+      if (p.mode == 0) {
+        const QamParams qp{p.qb, p.levels, p.qscale};
+        float2* sdst = p.s_hat + sym_base + t;
+        uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const float dd = fmaxf(den[i], p.eps);  // np.maximum(den, eps)
+          const float2 shv = make_float2(a[2 * i] / dd, a[2 * i + 1] / dd);
+          if (!isfinite(shv.x) || !isfinite(shv.y)) flag |= 1u;
+          const int j = shifted_bin<M>(i, 0);
+          sdst[j] = shv;
+          demap_store(shv, qp, bdst + (long long)j * p.qb);
+        }
+      } else {
+        float2* ndst = p.part_num + sym_base + t;
+        if (p.num_dst != nullptr) {
+          const int o = f / p.fpo;
+          ndst = p.num_dst[o] + (((long long)p.slot * p.fpo + (f - o * p.fpo)) * D + d_own) * M + t;
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          if (!isfinite(a[2 * i]) || !isfinite(a[2 * i + 1])) flag |= 1u;
+          ndst[shifted_bin<M>(i, 0)] = make_float2(a[2 * i], a[2 * i + 1]);
+        }
+      }
     }
   }
   if (flag != 0u && p.flags != nullptr) atomicOr(&p.flags[f], flag);
+  // remote readers of this CTA's partials are done before it exits
   tmem_fence_before();
-  __syncthreads();
+  cluster_arrive();
+  cluster_wait();
   tmem_fence_after();
-  if (w == 0) tmem_dealloc(*tmem_slot, 512);
+  if (w == 0) tmem_dealloc(*tmem_slot, cols);
+  if (p.num_dst != nullptr && threadIdx.x == 0) __threadfence_system();  // peer stores before the exchange flags
+}
+
+template <int M, bool BPSK, bool ZF>
+cudaError_t launch_t(const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
+  using BC = BalCfg<M>;
+  static unsigned done = 0;
+  auto kern = rx_balanced_kernel<M, BPSK, ZF>;
+  if (cudaError_t e = ensure_smem_attr(kern, (int)BC::smem_bytes(BC::LPC_MAX), done); e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.n_frames * (unsigned)bp.cluster, 1, 1);
+  cfg.blockDim = dim3((unsigned)(bp.lanes_per_cta * BC::G), 1, 1);
+  // CTAs of one cluster may share an SM; every CTA allocates TMEM (blocking
+  // tcgen05.alloc), so more co-resident CTAs than the SM's 512 columns hold
+  // could wait forever on cluster-mates parked at a cluster barrier.  Pad the
+  // shared memory request so that at most 512 / cols CTAs fit on an SM.
+  const int nw = bp.lanes_per_cta * BC::LW;
+  unsigned cols = 32;
+  while (cols < (unsigned)(((nw + 3) / 4) * BC::COLS)) cols <<= 1;
+  const size_t per_sm = 228 * 1024, fit = 512 / cols;
+  size_t smem = BC::smem_bytes(bp.lanes_per_cta);
+  if (smem < per_sm / (fit + 1) + 1) smem = per_sm / (fit + 1) + 1;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)bp.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int M>
+cudaError_t launch_m(const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
+  const bool zf = p.zf != nullptr;
+  if (p.pilot_bpsk) return zf ? launch_t<M, true, true>(p, bp, s) : launch_t<M, true, false>(p, bp, s);
+  return zf ? launch_t<M, false, true>(p, bp, s) : launch_t<M, false, false>(p, bp, s);
+}
+
+template <int M>
+bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
+  using BC = BalCfg<M>;
+  constexpr int LMAX = BC::LPC_MAX;
+  // V (virtual lanes per frame) depends on the frame shape only: ~64 rows
+  // per lane, and at least D lanes so that a lane's range (<= D*N/V rows)
+  // never spans more than two symbols
+  const long long rows = (long long)n_ant * (1 + n_data);
+  int c = (int)((rows + 64LL * LMAX - 1) / (64LL * LMAX));
+  if (c < 1) c = 1;
+  while (c * LMAX < n_data) ++c;
+  if (c > BMAX_CLUSTER) return false;
+  const int V = c * LMAX;
+  // CTA mapping depends on the batch: the fewest CTAs per frame (largest
+  // lpc) that still give every SM a CTA, within the portable cluster size
+  int best_lpc = LMAX;
+  for (int lpc = LMAX; lpc >= 1; --lpc) {
+    if (V % lpc != 0 || V / lpc > BMAX_CLUSTER) continue;
+    best_lpc = lpc;
+    if ((long long)n_frames * (V / lpc) >= n_sm) break;
+  }
+  out->workers = V;
+  out->lanes_per_cta = best_lpc;
+  out->cluster = V / best_lpc;
+  out->fft_lane_threads = BC::G;
+  return true;
 }
 
 }  // namespace
 
-bool balanced_eligible(int M, int n_ant, int n_data, int mode, bool zf, int shards) {
+bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
 #ifdef OFDMRX_NO_BALANCED
   return false;
 #else
-  return M == BM && mode == 0 && !zf && shards == 1 && n_data >= 1 && n_data <= BW && n_ant >= 1;
+  if (n_ant < 1 || n_data < 0) return false;
+  switch (M) {
+    case 1024: return plan_m<1024>(n_ant, n_data, n_frames, n_sm, out);
+    case 2048: return plan_m<2048>(n_ant, n_data, n_frames, n_sm, out);
+    case 4096: return plan_m<4096>(n_ant, n_data, n_frames, n_sm, out);
+    default: return false;
+  }
 #endif
 }
 
-size_t balanced_smem_bytes() { return BBAR + (size_t)BW * 2 * BSS * sizeof(float2); }
+size_t balanced_smem_bytes(int M, int lanes_per_cta) {
+  switch (M) {
+    case 1024: return BalCfg<1024>::smem_bytes(lanes_per_cta);
+    case 2048: return BalCfg<2048>::smem_bytes(lanes_per_cta);
+    case 4096: return BalCfg<4096>::smem_bytes(lanes_per_cta);
+    default: return 0;
+  }
+}
 
-cudaError_t launch_balanced(const FusedParams& p, cudaStream_t s) {
+cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
   if (p.n_frames == 0) return cudaSuccess;
-  static unsigned done_t = 0, done_f = 0;
-  const size_t smem = balanced_smem_bytes();
-  cudaError_t e = ensure_smem_attr(rx_balanced_kernel<true>, (int)smem, done_t);
-  if (e == cudaSuccess) e = ensure_smem_attr(rx_balanced_kernel<false>, (int)smem, done_f);
-  if (e != cudaSuccess) return e;
-  if (p.pilot_bpsk) rx_balanced_kernel<true><<<p.n_frames, BW * 32, smem, s>>>(p);
-  else rx_balanced_kernel<false><<<p.n_frames, BW * 32, smem, s>>>(p);
-  return cudaGetLastError();
+  switch (M) {
+    case 1024: return launch_m<1024>(p, bp, s);
+    case 2048: return launch_m<2048>(p, bp, s);
+    case 4096: return launch_m<4096>(p, bp, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace ofdmrx

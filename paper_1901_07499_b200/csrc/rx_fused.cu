@@ -405,7 +405,7 @@ static cudaError_t plan_impl(int n_frames, int n_data, FusedLaunch* l) {
   if (ngroups < 1) ngroups = 1;
   while (ngroups > 1 && FC::smem_bytes(ngroups, per_group) > smem_cap) --ngroups;
   const long long n_work = (long long)n_frames * chunks;
-  const long long want = (n_work + 148LL * GI - 1) / (148LL * GI);  // spread groups over the 148 SMs first
+  const long long want = (n_work + (long long)device_sm_count() * GI - 1) / ((long long)device_sm_count() * GI);  // spread groups over the SMs first
   if (ngroups > want) ngroups = (int)(want < 1 ? 1 : want);
   l->dc = dc;
   l->npilot = npilot;

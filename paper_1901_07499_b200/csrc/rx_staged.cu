@@ -57,7 +57,7 @@ static cudaError_t fft_rows_impl(const FftRowsParams& p, cudaStream_t s) {
   const long long rows = (long long)p.n_frames * p.n_sym * p.n_ant;
   if (rows == 0) return cudaSuccess;
   long long blocks = (rows + lanes - 1) / lanes;
-  const long long cap = 148LL * 16;
+  const long long cap = (long long)device_sm_count() * 16;
   const int grid = (int)(blocks < cap ? blocks : cap);
   const int iters = (int)((blocks + grid - 1) / grid);
   fft_rows_kernel<M><<<grid, threads, smem, s>>>(p, lanes, iters);
@@ -101,7 +101,7 @@ cudaError_t launch_ls(const float2* Y, long long y_fs, int n_frames, int n_ant, 
   const long long total = (long long)n_frames * n_ant * M;
   if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > device_sm_count() * 32) blocks = device_sm_count() * 32;
   ls_kernel<<<(int)blocks, 256, 0, s>>>(Y, y_fs, n_frames, n_ant, M, pilot, H);
   return cudaGetLastError();
 }
@@ -176,7 +176,7 @@ cudaError_t launch_mrc(const MrcParams& p, cudaStream_t s) {
   const long long total = (long long)p.n_frames * p.n_data * p.M;
   if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > device_sm_count() * 32) blocks = device_sm_count() * 32;
   mrc_kernel<<<(int)blocks, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
@@ -193,7 +193,7 @@ cudaError_t launch_demap(const float2* sym, long long n, int qb, int levels, flo
                          cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   long long blocks = (n + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > device_sm_count() * 32) blocks = device_sm_count() * 32;
   demap_kernel<<<(int)blocks, 256, 0, s>>>(sym, n, QamParams{qb, levels, scale}, bits);
   return cudaGetLastError();
 }
@@ -211,6 +211,8 @@ __global__ void finish_kernel(const FinishParams p) {
     const int k = (int)(i % p.M);
     const long long f = i / ((long long)p.n_data * p.M);
     const long long di = f * p.M + k;
+    // frames a detection rejected (NOT_DETECTED / OUT_OF_RANGE) carry no partials
+    if (p.flags != nullptr && (p.flags[f] & 12u) != 0u) continue;
     float sr[32], si[32], sd[32];
     int top = 0;
     for (int g = 0; g < p.parts; ++g) {
@@ -251,7 +253,7 @@ cudaError_t launch_finish(const FinishParams& p, cudaStream_t s) {
   const long long total = (long long)p.n_frames * p.n_data * p.M;
   if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > device_sm_count() * 32) blocks = device_sm_count() * 32;
   finish_kernel<<<(int)blocks, 256, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -395,7 +395,7 @@ cudaError_t launch_corr_fft(const SyncParams& p, float2* cspec, int bound_mode, 
   const long long bpr = (p.wins + L - 1) / L;
   const long long total = (long long)p.n_frames * p.n_ant * bpr;
   long long grid = (total + CF_LANES - 1) / CF_LANES;
-  if (grid > 148LL * 2 * 8) grid = 148LL * 2 * 8;  // persistent-ish: blocks of a row stay on one lane
+  if (grid > (long long)device_sm_count() * 2 * 8) grid = (long long)device_sm_count() * 2 * 8;  // persistent-ish: blocks of a row stay on one lane
   corr_fft_kernel<<<(unsigned)grid, 32 * CF_LANES, smem, s>>>(p, cspec, bpr, bound_mode);
   return cudaGetLastError();
 }

@@ -244,7 +244,7 @@ cudaError_t launch_synth_bits(uint8_t* bits, long long n_per_frame, int n_frames
   const long long total = n_per_frame * n_frames;
   if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks > device_sm_count() * 64) blocks = device_sm_count() * 64;
   bits_kernel<<<(unsigned)blocks, 256, 0, s>>>(bits, n_per_frame, n_frames, seed);
   return cudaGetLastError();
 }

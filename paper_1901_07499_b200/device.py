@@ -63,10 +63,12 @@ def qam_bits(order):
 
 
 def make_desc(n_frames, n_antennas, fft_len, cp_len, n_data, qam_order, symbol0_offset, row_stride,
-              frame_stride, eps=MRC_WEIGHT_FLOOR, options=0):
+              frame_stride, eps=MRC_WEIGHT_FLOOR, options=0, *, rx_samples):
+    """ofdmrx_frame_desc; rx_samples = complex samples readable at the capture
+    pointer (the C side bounds-checks every call against it)."""
     return _lib.FrameDesc(int(n_frames), int(n_antennas), int(fft_len), int(cp_len), int(n_data),
                           int(qam_order), int(symbol0_offset), int(row_stride), int(frame_stride),
-                          float(eps), int(options))
+                          float(eps), int(options), int(rx_samples))
 
 
 def pilot_options(pilot_values):
@@ -75,10 +77,20 @@ def pilot_options(pilot_values):
     return _lib.OPT_PILOT_BPSK if np.all((v.imag == 0) & (np.abs(v.real) == 1)) else 0
 
 
-def check_desc(desc, rx_len=-1):
+def check_desc(desc):
     import ctypes
 
-    _lib.check(_lib.load().ofdmrx_check_desc(ctypes.byref(desc), int(rx_len)))
+    _lib.check(_lib.load().ofdmrx_check_desc(ctypes.byref(desc)))
+
+
+def rx_plan(desc, mode=0):
+    """ofdmrx_rx_plan: the kernel, worker count (antenna-sum order) and CTA
+    mapping a fused call with this descriptor uses on the current device."""
+    import ctypes
+
+    out = _lib.Plan()
+    _lib.check(_lib.load().ofdmrx_rx_plan(ctypes.byref(desc), int(mode), 0, ctypes.byref(out)))
+    return {name: getattr(out, name) for name, _ in _lib.Plan._fields_}
 
 
 # ---------------------------------------------------------------------------
@@ -96,7 +108,7 @@ def fft_shift_rows(rows, device=None, stream=None):
     r, m = x.shape
     out = torch.empty((r, m), dtype=torch.complex64, device=dev)
     # rows as frames of one antenna and one symbol without CP
-    desc = make_desc(r, 1, m, 0, 0, 4, 0, m, m)
+    desc = make_desc(r, 1, m, 0, 0, 4, 0, m, m, rx_samples=r * m)
     _lib.call("ofdmrx_fft_shift", ctypes.byref(desc), 0, 1, ptr(x), ptr(out), stream_handle(stream))
     return out
 

@@ -90,12 +90,14 @@ def allocate_outputs(n_frames, n_antennas, fft_len, n_data, qam_order, dev, want
 
 
 def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
-                   out=None, want_h=True, zf=False, check=False, stream=None, shards=True):
+                   out=None, want_h=True, zf=False, check=False, stream=None, shards=None):
     """Fused receive of a batch of captures on the current CUDA device.
 
     rx: complex64 CUDA tensor [F, N, S] or [N, S] (numpy is copied H2D).
     Returns a FrameBatch.  With check=True, raises NumericInputError when a
-    frame fed non-finite samples to the FFT (forces a device sync)."""
+    frame fed non-finite samples to the FFT (forces a device sync).  Results
+    do not depend on the batch (F) a frame is received in; `shards` is
+    accepted for compatibility and ignored."""
     if not isinstance(cfg, OfdmConfig):
         raise ContractError("cfg must be an OfdmConfig")
     dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
@@ -113,14 +115,14 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     if n_data < 0 or symbol0_offset < 0:
         raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
     desc_args = (f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
-    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards)
+    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream)
 
 
-def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards=True):
+def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards=None):
     f, n, _, _, n_data = desc_args[:5]
     pvals = _pilot_values(pilot, cfg.fft_len)
-    desc = device.make_desc(*desc_args, options=device.pilot_options(pvals) | (0 if shards else _lib.OPT_NO_SHARDS))
-    device.check_desc(desc, x.numel())
+    desc = device.make_desc(*desc_args, options=device.pilot_options(pvals), rx_samples=x.numel())
+    device.check_desc(desc)
     pv = _PILOTS.get(pvals, x.device)
     if out is None:
         out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, x.device, want_h=want_h, zf=zf)
@@ -154,8 +156,9 @@ def stage_symbols(src, cfg, *, symbol0_offset=0, n_data, dst=None, stream=None):
         dst = torch.empty((f, n, 1 + n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
     if tuple(dst.shape) != (f, n, 1 + n_data, cfg.fft_len) or not dst.is_contiguous():
         raise ContractError(f"dst must be contiguous [{f}, {n}, {1 + n_data}, {cfg.fft_len}]")
-    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s)
-    device.check_desc(desc, f * n * s)
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s,
+                            rx_samples=f * n * s)
+    device.check_desc(desc)
     _lib.call("ofdmrx_stage_symbols", ctypes.byref(desc), device.ctypes_void(src.data_ptr()), device.ptr(dst),
               device.stream_handle(stream))
     return dst
@@ -188,8 +191,8 @@ def receive_partials(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=
         n_data = (s - symbol0_offset) // cfg.symbol_len - 1
     pvals = _pilot_values(pilot, cfg.fft_len)
     desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps,
-                            options=device.pilot_options(pvals))
-    device.check_desc(desc, f * n * s)
+                            options=device.pilot_options(pvals), rx_samples=x.numel())
+    device.check_desc(desc)
     pv = _PILOTS.get(pvals, dev)
     H = torch.empty((f, n, cfg.fft_len), dtype=torch.complex64, device=dev) if want_h else None
     num = torch.empty((f, n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
@@ -230,8 +233,9 @@ def fft_symbols(rx, cfg, *, symbol0_offset=0, n_data=None, first_symbol=0, n_sym
         n_data = (s - symbol0_offset) // cfg.symbol_len - 1
     if n_symbols is None:
         n_symbols = 1 + n_data - first_symbol
-    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s)
-    device.check_desc(desc, f * n * s)
+    desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s,
+                            rx_samples=x.numel())
+    device.check_desc(desc)
     y = torch.empty((f, n_symbols, n, cfg.fft_len), dtype=torch.complex64, device=dev)
     _lib.call("ofdmrx_fft_shift", ctypes.byref(desc), int(first_symbol), int(n_symbols), device.ptr(x),
               device.ptr(y), device.stream_handle(stream))
@@ -303,7 +307,7 @@ def _slice_batch(out, n):
 
 
 def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, eps=device.MRC_WEIGHT_FLOOR,
-                     want_h=True, zf=False, shards=True, antennas="first", stream=None):
+                     want_h=True, zf=False, shards=None, antennas="first", stream=None):
     """Raw captures -> bits with the packet timing found on the device.
 
     The reference's detect_packet -> extract_slots -> run_ring_pipeline chain
@@ -332,7 +336,7 @@ def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, ep
     det = sync.detect_frames(x, chips, thr, antennas=antennas, stream=stream)
     pvals = _pilot_values(pilot, cfg.fft_len)
     desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, 0, s, n * s, eps,
-                            options=device.pilot_options(pvals) | (0 if shards else _lib.OPT_NO_SHARDS))
+                            options=device.pilot_options(pvals), rx_samples=x.numel())
     pv = _PILOTS.get(pvals, dev)
     out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
     _lib.call("ofdmrx_rx_frames_detected", ctypes.byref(desc), s, device.ptr(det.peak_index),

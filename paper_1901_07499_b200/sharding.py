@@ -243,7 +243,7 @@ class AntennaShardedReceiver:
         _lib.check(lib.ofdmrx_peer_wait(dv.ptr(ex.consumed_src), g, e - 1, st))
         pvals = frames._pilot_values(self.pilot, m)
         desc = dv.make_desc(f, n, m, self.cfg.cp_len, d, self.cfg.qam_order, self.symbol0_offset, s, n * s,
-                            options=dv.pilot_options(pvals))
+                            options=dv.pilot_options(pvals), rx_samples=x.numel())
         H = torch.empty((f, n, m), dtype=torch.complex64, device=x.device) if want_h else None
         flags = torch.zeros((f,), dtype=torch.int32, device=x.device)
         pv = frames._PILOTS.get(pvals, x.device)

@@ -1,6 +1,6 @@
 """A/B timing of the fused receive kernel (developer tool, not the bench).
 
-    OFDMRX_LIB=build/variants/libofdmrx_b200_X.so python scripts/fused_quick.py [C3] [frames]
+    OFDMRX_VARIANT_LIB=build/variants/libofdmrx_b200_X.so python scripts/fused_quick.py [C3] [frames]
 
 Prints ms per launch, µs per frame and the fraction of the measured HBM peak
 (algorithmic bytes), plus BER of the tiled frames vs truth."""
@@ -13,7 +13,10 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
-from paper_1901_07499_b200 import frames  # noqa: E402
+from paper_1901_07499_b200 import _lib, frames  # noqa: E402
+
+if os.environ.get("OFDMRX_VARIANT_LIB"):  # experiment build (build.py --variant); the package itself never does this
+    _lib.LIB_PATH = os.environ["OFDMRX_VARIANT_LIB"]
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 n, m, cp, qam, d, F = bench.CONFIGS[cfg_name]
@@ -36,5 +39,5 @@ torch.cuda.synchronize()
 ms = a.elapsed_time(b) / reps
 peak, _ = bench.load_peaks()
 bpf = bench.frame_bytes(n, m, qam, d)
-print(json.dumps({"lib": os.environ.get("OFDMRX_LIB", "in-tree"), "cfg": cfg_name, "frames": F, "reps": reps, "ms": ms,
+print(json.dumps({"lib": os.environ.get("OFDMRX_VARIANT_LIB", "in-tree"), "cfg": cfg_name, "frames": F, "reps": reps, "ms": ms,
                   "us_per_frame": ms * 1e3 / F, "frac": bpf * F / (ms * 1e-3) / 1e9 / peak, "ber": ber}))

@@ -1,8 +1,8 @@
 """Randomised parity sweep of ofdmrx_rx_frames against the oracle: FFT sizes
 2..4096, 1..70 antennas, 0..14 data symbols, every QAM order, random CP,
-symbol0 offsets (odd sample offsets included), padded rows, ZF on/off and
-on-device shards on/off, so every kernel path (rx_balanced, rx_fused,
-sharded + finish) meets the same bar: bits exact, H / s_hat / weights within
+symbol0 offsets (odd sample offsets included), padded rows and ZF on/off,
+so every kernel path (rx_balanced at any cluster mapping, rx_fused) meets
+the same bar: bits exact, H / s_hat / weights within
 1e-4 relative.  Fixed seed: the same 36 configurations every run."""
 
 import math

@@ -76,17 +76,31 @@ def test_fused_vs_oracle(P, case):
     assert int(out.flags.abs().sum()) == 0
 
 
-@pytest.mark.parametrize("name", ["C1", "C1_0dB", "C2", "C3", "C4"])
-def test_fused_vs_reference_golden(P, golden_dir, name):
-    """Directly against vectors produced by the reference itself."""
+GOLDEN_SETS = ["C1", "C1_0dB", "C2", "C3", "C3_0dB", "C4", "C4_0dB"]
+
+
+@pytest.mark.parametrize("tile", [1, 160], ids=["alone", "batch160"])
+@pytest.mark.parametrize("name", GOLDEN_SETS)
+def test_fused_vs_reference_golden(P, golden_dir, name, tile):
+    """Directly against vectors produced by the reference itself, with the
+    frame received alone (F = 1, spread over a cluster for M >= 1024) and
+    tiled into a 160-frame batch (one CTA per frame: the benched mapping)."""
     g = dict(np.load(os.path.join(golden_dir, f"frames_{name}.npz")))
     n_ant, m, cp, qam, d = (int(v) for v in g["spec"])
+    if tile > 1 and n_ant * m > 64 * 1024:
+        tile = 40  # C4: 40 x 52 MB
     cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
     for f in g["seeds"]:
         tag = f"f{int(f)}"
         streams, _, s0 = orc.synth_capture(m, cp, n_ant, qam, d, int(f), snr_db=float(g["snr_db"]))
-        out = P.receive_frames(torch.from_numpy(streams.astype(np.complex64)).cuda(), cfg,
-                               symbol0_offset=s0, n_data=d)
+        x = torch.from_numpy(streams.astype(np.complex64)).cuda()[None].repeat(tile, 1, 1).contiguous()
+        out = P.receive_frames(x, cfg, symbol0_offset=s0, n_data=d)
+        torch.cuda.synchronize()
+        if tile > 1:  # every copy identical, then check copy `tile - 1` below
+            assert torch.equal(out.bits, out.bits[:1].expand_as(out.bits))
+            assert torch.equal(out.s_hat, out.s_hat[:1].expand_as(out.s_hat))
+            out = type(out)(H=out.H[tile - 1:], s_hat=out.s_hat[tile - 1:], weights=out.weights[tile - 1:],
+                            bits=out.bits[tile - 1:], flags=out.flags[tile - 1:])
         ref_bits = np.unpackbits(g[f"{tag}_bits"])[: d * m * cfg.bits_per_qam_symbol]
         assert np.array_equal(out.bits[0].cpu().numpy(), ref_bits)
         assert rel(out.s_hat[0].cpu().numpy(), g[f"{tag}_s_hat"]) < REL_TOL
@@ -350,7 +364,8 @@ def test_stage_symbols_drops_cp_and_matches_full_receive(P, layout):
 
         base = big.pin_memory()
         dst = torch.empty((nf, n_ant, 1 + d, m), dtype=torch.complex64, device="cuda")
-        desc = device.make_desc(nf, n_ant, m, cp, d, qam, s0, streams.shape[2], (n_ant + 1) * streams.shape[2])
+        desc = device.make_desc(nf, n_ant, m, cp, d, qam, s0, streams.shape[2], (n_ant + 1) * streams.shape[2],
+                                rx_samples=base.numel())
         _lib.call("ofdmrx_stage_symbols", ctypes.byref(desc), device.ctypes_void(base.data_ptr()), device.ptr(dst),
                   device.stream_handle())
     else:
@@ -396,15 +411,32 @@ def test_fused_complex_unit_pilot(P, n_ant, m, cp, qam, d, nf):
         assert rel(out.weights[f].cpu().numpy(), w) < REL_TOL
 
 
-@pytest.mark.parametrize("n_ant,d,nf,bpsk", [(64, 10, 3, True), (8, 12, 2, True), (5, 3, 2, True), (100, 1, 2, True),
-                                             (13, 7, 2, False), (1, 12, 2, True), (64, 10, 2, False)])
-def test_balanced_kernel_m1024(P, n_ant, d, nf, bpsk):
-    """M = 1024 frames with one CTA per frame (no on-device shards): the
-    balanced kernel (rx_balanced.cu: pilot rows first, data rows split evenly
-    over the 12 warps, H through L2, symbols spanning warps combined in the
-    epilogue).  Covers ranges exactly N rows long, warps without rows, N < 12
-    and a single antenna."""
-    m, cp, qam = 1024, 72, 16
+BALANCED_CASES = [
+    # (M, N, D, frames, BPSK pilot)
+    (1024, 64, 10, 3, True), (1024, 8, 12, 2, True), (1024, 5, 3, 2, True), (1024, 100, 1, 2, True),
+    (1024, 13, 7, 2, False), (1024, 1, 12, 2, True), (1024, 64, 10, 2, False),
+    # D*N < workers: empty lanes sit between a symbol's owner and the lanes
+    # continuing it (the owner must skip them, not stop)
+    (1024, 2, 1, 2, True), (1024, 4, 2, 2, True), (1024, 10, 1, 2, True), (1024, 2, 5, 2, True),
+    (1024, 3, 2, 1, True), (1024, 6, 1, 1, True), (1024, 7, 1, 1, True),
+    # more data symbols than one CTA's lanes: the frame's workers span a cluster
+    (1024, 16, 20, 2, True), (1024, 3, 40, 1, True),
+    # M = 2048 (lanes of 64 threads) and M = 4096 (128 threads)
+    (2048, 32, 10, 2, True), (2048, 3, 4, 2, True), (2048, 7, 1, 1, False), (2048, 256, 2, 1, True),
+    (4096, 5, 3, 2, True), (4096, 1, 2, 1, True), (4096, 9, 6, 1, False),
+]
+
+
+@pytest.mark.parametrize("m,n_ant,d,nf,bpsk", BALANCED_CASES, ids=lambda c: str(c))
+def test_balanced_kernel(P, m, n_ant, d, nf, bpsk):
+    """The balanced kernel (rx_balanced.cu: pilot rows first, data rows split
+    evenly over the frame's workers, H through L2, symbols spanning workers
+    combined in the epilogue, over DSMEM when the workers span a cluster) at
+    every batch mapping: frames received together and one at a time."""
+    from paper_1901_07499_b200 import device
+
+    cp = m // 8
+    qam = 16
     pilot = orc.make_pilot(m) if bpsk else np.exp(2j * np.pi * np.random.default_rng(n_ant).random(m))
     caps = []
     for f in range(nf):
@@ -414,10 +446,15 @@ def test_balanced_kernel_m1024(P, n_ant, d, nf, bpsk):
         caps.append(st)
     streams = np.stack(caps)
     cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    x = torch.from_numpy(streams.astype(np.complex64)).cuda()
+    desc = device.make_desc(nf, n_ant, m, cp, d, qam, 255, x.shape[2], n_ant * x.shape[2], rx_samples=x.numel())
+    assert device.rx_plan(desc)["kernel"] == 1  # OFDMRX_KERNEL_BALANCED
     for want_h in (True, False):
-        out = P.receive_frames(torch.from_numpy(streams.astype(np.complex64)).cuda(), cfg, pilot,
-                               symbol0_offset=255, n_data=d, shards=False, want_h=want_h)
+        outs = [P.receive_frames(x, cfg, pilot, symbol0_offset=255, n_data=d, want_h=want_h)]
+        outs += [P.receive_frames(x[f:f + 1], cfg, pilot, symbol0_offset=255, n_data=d, want_h=want_h)
+                 for f in range(nf)]
         torch.cuda.synchronize()
+        out = outs[0]
         assert int(out.flags.abs().sum()) == 0
         for f in range(nf):
             H, s_hat, w, bits = orc.receive_frame(streams[f], 255, m, cp, d, qam, pilot=pilot)
@@ -426,3 +463,5 @@ def test_balanced_kernel_m1024(P, n_ant, d, nf, bpsk):
             assert rel(out.weights[f].cpu().numpy(), w) < REL_TOL
             if want_h:
                 assert rel(out.H[f].cpu().numpy(), H) < REL_TOL
+            single = outs[1 + f]
+            assert torch.equal(single.bits[0], out.bits[f]) and torch.equal(single.s_hat[0], out.s_hat[f])

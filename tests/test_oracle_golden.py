@@ -58,7 +58,7 @@ def test_pilot_pn_and_modulate(unit):
     assert np.array_equal(orc.ofdm_modulate(orc.make_pilot(64), 16)[0], unit["pilot_symbol_64"])
 
 
-FRAME_SETS = ["C1", "C1_0dB", "C2", "C3", "C4"]
+FRAME_SETS = ["C1", "C1_0dB", "C2", "C3", "C3_0dB", "C4", "C4_0dB"]
 
 
 @pytest.mark.parametrize("name", FRAME_SETS)
