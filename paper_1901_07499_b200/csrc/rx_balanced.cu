@@ -10,14 +10,15 @@
 //            accumulated into the lane's den partial (TMEM);
 //            cluster barrier ARRIVE (release: H rows published)
 //   phase B  the D x N data rows, symbol-major (antennas ascending inside a
-//            symbol), are cut into V equal contiguous ranges (<= N rows each,
-//            so a lane touches at most 2 symbols).  A lane streams its range:
+//            symbol), are cut into V contiguous ranges that even out the
+//            lanes' pilot + data rows (<= N rows each, so a lane touches at
+//            most 2 symbols).  A lane streams its range:
 //            the next rx row is TMA-prefetched, and once the FFT's last pass
 //            has its inputs the lane loads H_n from L2 into registers
 //            (ld.global.cg) so the latency hides under that pass.  The first
-//            of these loads is preceded by the cluster barrier WAIT (acquire),
-//            so a lane that finished its pilot rows early runs its first data
-//            FFT instead of idling.  MRC accumulators (<= 2 symbols) in TMEM.
+//            of these loads is preceded by the cluster barrier WAIT (acquire;
+//            an mbarrier when the frame has one CTA), so a lane that finished
+//            its pilot rows early runs its first data FFT instead of idling.  MRC accumulators (<= 2 symbols) in TMEM.
 //   epilogue den = sum of the V lane partials in lane order; the owner of
 //            each symbol (the lane holding its first row) adds the partials
 //            of the lanes continuing it, in lane order, then divides, demaps
@@ -50,7 +51,26 @@ struct BalCfg {
   static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * SLOT * sizeof(float2); }
 };
 
-__device__ __forceinline__ int range_lo(int v, int total, int V) { return (int)((long long)total * v / V); }
+// pilot rows of lane q (rows n = q, q + V, ... < N)
+__device__ __forceinline__ int pilots_of(int q, int N, int V) { return q < N ? (N - 1 - q) / V + 1 : 0; }
+
+// First data row of lane v.  The frame's N(1+D) rows are split evenly over
+// the V lanes counting each lane's pilot rows, so the lanes that FFT one
+// pilot row more get one data row less; boundaries are the prefix maximum of
+// that split (monotone even when a lane's pilot share exceeds its total).
+// A lane's range is at most ceil(N(1+D)/V) <= N rows when V > D.
+__device__ int range_lo(int v, int N, int D, int V) {
+  const int total = D * N;
+  if (v >= V) return total;
+  const long long rows = (long long)N * (1 + D);
+  int best = 0, pc = 0;
+  for (int q = 0; q <= v; ++q) {
+    const int g = (int)(rows * q / V) - pc;
+    best = g > best ? g : best;
+    pc += pilots_of(q, N, V);
+  }
+  return best < total ? best : total;
+}
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -106,7 +126,9 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     return;
   }
   uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [lpc][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rx_bar + 2 * BC::LPC_MAX);
+  uint64_t* h_bar = rx_bar + 2 * BC::LPC_MAX;                 // H rows published (one-CTA frames)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_bar + 1);
+  const bool one_cta = V == lpc;
   float2* slot_base = reinterpret_cast<float2*>(smem_raw + BBAR) + (size_t)l * 2 * SS;
   const bool leader = t == 0;
   auto lane_sync = [&]() {
@@ -115,6 +137,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   };
 
   if (threadIdx.x < 2 * lpc) mbar_init(&rx_bar[threadIdx.x], 1);
+  if (threadIdx.x == 0) mbar_init(h_bar, blockDim.x);
   fence_mbar_init();
   const int nw = lpc * LW;
   uint32_t cols = 32;
@@ -156,7 +179,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     tmem_st<ACC>(tbase + ACC, z);
   }
   const int total = D * N;
-  const int r0 = range_lo(v, total, V), r1 = range_lo(v + 1, total, V);
+  const int r0 = range_lo(v, N, D, V), r1 = range_lo(v + 1, N, D, V);
   int k = 0;  // stage counter across both phases
   if (leader && v < N) issue_rx(row_addr(0, v), 0);
   float2 y[P];
@@ -196,9 +219,19 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   }
   if (leader && v >= N && r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), k & 1);  // no pilot rows
   tmem_wait_st();
-  // H rows of this lane are published; lanes of the cluster acquire them
-  // before their first H load (wait inside the first data FFT, below)
-  cluster_arrive();
+  // H rows of this lane are published; lanes of the frame acquire them
+  // before their first H load (wait inside the first data FFT, below).  One
+  // CTA: an mbarrier (release / acquire at CTA scope); a cluster: the split
+  // cluster barrier.
+  auto h_publish = [&] {
+    if (one_cta) mbar_arrive_cta(h_bar);
+    else cluster_arrive();
+  };
+  auto h_acquire = [&] {
+    if (one_cta) mbar_wait_parity(h_bar, 0u);
+    else cluster_wait();
+  };
+  h_publish();
   bool h_acquired = false;
 
   // ---------------- phase B: this lane's data rows -------------------------
@@ -220,7 +253,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     const float2* hsrc = Hf + (long long)n * M + t;
     fft_forward<M>(y, slot, t, [&](int idx) { return src[idx]; }, lane_sync, [&] {
       if (!h_acquired) {
-        cluster_wait();
+        h_acquire();
         h_acquired = true;
       }
 #pragma unroll
@@ -260,7 +293,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     d = dn, n = nn;
     if (++nn == N) nn = 0, ++dn;
   }
-  if (!h_acquired) cluster_wait();
+  if (!h_acquired) h_acquire();
 
   // ---------------- epilogue -------------------------------------------------
   // every lane parks its den partial (and the partial of a symbol it
@@ -287,8 +320,15 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
       for (int i = 0; i < P; ++i) partbuf[l * M + i * G + t] = make_float2(a[2 * i], a[2 * i + 1]);
     }
   }
-  cluster_arrive();
-  cluster_wait();
+  auto frame_sync = [&] {  // all lanes of the frame (CTA or cluster)
+    if (one_cta) {
+      __syncthreads();
+    } else {
+      cluster_arrive();
+      cluster_wait();
+    }
+  };
+  frame_sync();
 
   // the symbol owned by this lane: its first row lies in [r0, r1)
   const int d_own = has_rows ? (r0 + N - 1) / N : D;
@@ -337,7 +377,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
       // add the partials of the following lanes that continue this symbol, in
       // lane order; lanes without rows are skipped (N < V leaves some empty)
       for (int q = v + 1; q < V; ++q) {
-        const int q0 = range_lo(q, total, V), q1 = range_lo(q + 1, total, V);
+        const int q0 = range_lo(q, N, D, V), q1 = range_lo(q + 1, N, D, V);
         if (q0 >= q1) continue;
         if (q0 / N != d_own || q0 % N == 0) break;
         const uint32_t rk = (uint32_t)(q / lpc);
@@ -390,8 +430,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   if (flag != 0u && p.flags != nullptr) atomicOr(&p.flags[f], flag);
   // remote readers of this CTA's partials are done before it exits
   tmem_fence_before();
-  cluster_arrive();
-  cluster_wait();
+  frame_sync();
   tmem_fence_after();
   if (w == 0) tmem_dealloc(*tmem_slot, cols);
   if (p.num_dst != nullptr && threadIdx.x == 0) __threadfence_system();  // peer stores before the exchange flags
@@ -439,13 +478,13 @@ template <int M>
 bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
   using BC = BalCfg<M>;
   constexpr int LMAX = BC::LPC_MAX;
-  // V (virtual lanes per frame) depends on the frame shape only: ~64 rows
-  // per lane, and at least D lanes so that a lane's range (<= D*N/V rows)
-  // never spans more than two symbols
-  const long long rows = (long long)n_ant * (1 + n_data);
-  int c = (int)((rows + 64LL * LMAX - 1) / (64LL * LMAX));
-  if (c < 1) c = 1;
-  while (c * LMAX < n_data) ++c;
+  // V (virtual lanes per frame) depends on the frame shape only: the fewest
+  // CTAs' worth of lanes with V > D, so that a lane's range (<= N(1+D)/V
+  // rows) never spans more than two symbols.  Few CTAs per frame keep the
+  // cluster small at large batches (a GPC fits fewer 8-CTA clusters than its
+  // SM count suggests, and the epilogue waits on every CTA of the frame).
+  (void)n_ant;
+  const int c = (n_data + 1 + LMAX - 1) / LMAX;
   if (c > BMAX_CLUSTER) return false;
   const int V = c * LMAX;
   // CTA mapping depends on the batch: the fewest CTAs per frame (largest
