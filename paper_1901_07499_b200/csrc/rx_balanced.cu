@@ -37,7 +37,8 @@ namespace ofdmrx {
 namespace {
 
 constexpr int BMAXW = 12;       // warps per CTA at most (register budget 168 x 384)
-constexpr size_t BBAR = 512;    // mbarriers + TMEM address word
+constexpr size_t BBAR = 1024;   // mbarriers, TMEM address word, range table
+constexpr int BMAX_V = 96;      // workers per frame at most (8 CTAs x 12 lanes)
 constexpr int BMAX_CLUSTER = 8; // portable cluster size
 
 template <int M>
@@ -51,25 +52,45 @@ struct BalCfg {
   static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * SLOT * sizeof(float2); }
 };
 
-// pilot rows of lane q (rows n = q, q + V, ... < N)
-__device__ __forceinline__ int pilots_of(int q, int N, int V) { return q < N ? (N - 1 - q) / V + 1 : 0; }
+// sum_{a=0}^{x} floor(a / V) (0 for x < 0)
+__device__ __forceinline__ long long floor_sum(long long x, int V) {
+  if (x < 0) return 0;
+  const long long k = x / V, r = x - k * V;
+  return V * k * (k - 1) / 2 + k * (r + 1);
+}
 
-// First data row of lane v.  The frame's N(1+D) rows are split evenly over
-// the V lanes counting each lane's pilot rows, so the lanes that FFT one
-// pilot row more get one data row less; boundaries are the prefix maximum of
-// that split (monotone even when a lane's pilot share exceeds its total).
-// A lane's range is at most ceil(N(1+D)/V) <= N rows when V > D.
-__device__ int range_lo(int v, int N, int D, int V) {
-  const int total = D * N;
-  if (v >= V) return total;
+// Data-row range table lo[0..V] of a frame: lane v streams data rows
+// [lo[v], lo[v+1]).  The N(1+D) rows are split evenly over the V lanes
+// counting each lane's pilot rows (n = q, q + V, ... < N), so the lanes that
+// FFT one pilot row more get one data row less; the boundaries are the
+// prefix maximum of that split (monotone even when a lane's pilot share
+// exceeds its total, N < V).  A range is at most ceil(N(1+D)/V) <= N rows
+// when V > D.  Built once per CTA by warp 0 (closed-form pilot counts and a
+// shuffle max-scan), so the hot loop and epilogue only read smem.
+__device__ void build_range_table(int* lo, int N, int D, int V) {
+  const int lane = threadIdx.x & 31;
   const long long rows = (long long)N * (1 + D);
-  int best = 0, pc = 0;
-  for (int q = 0; q <= v; ++q) {
-    const int g = (int)(rows * q / V) - pc;
-    best = g > best ? g : best;
-    pc += pilots_of(q, N, V);
+  const int total = D * N;
+  int carry = 0;
+  for (int base = 0; base <= V; base += 32) {
+    const int q = base + lane;
+    int g = 0;
+    if (q <= V) {
+      const int c = q < N ? q : N;  // lanes before q that own pilot rows
+      // pilots before q: sum_{q' < c} (floor((N-1-q')/V) + 1)
+      const long long pc = c + floor_sum(N - 1, V) - floor_sum((long long)N - 1 - c, V);
+      g = (int)(rows * q / V - pc);
+      if (q == V) g = total;
+    }
+    g = g > carry ? g : carry;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, g, o);
+      if (lane >= o && u > g) g = u;
+    }
+    if (q <= V) lo[q] = g < total ? g : total;
+    carry = __shfl_sync(0xffffffffu, g, 31);
   }
-  return best < total ? best : total;
 }
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -128,7 +149,12 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [lpc][2]
   uint64_t* h_bar = rx_bar + 2 * BC::LPC_MAX;                 // H rows published (one-CTA frames)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_bar + 1);
+  int* lo_tab = reinterpret_cast<int*>(smem_raw + 256);  // [V + 1]
+#ifdef OFDMRX_BAL_CLUSTER_BAR
+  const bool one_cta = false;  // experiment: the cluster barrier even for one-CTA frames
+#else
   const bool one_cta = V == lpc;
+#endif
   float2* slot_base = reinterpret_cast<float2*>(smem_raw + BBAR) + (size_t)l * 2 * SS;
   const bool leader = t == 0;
   auto lane_sync = [&]() {
@@ -139,6 +165,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   if (threadIdx.x < 2 * lpc) mbar_init(&rx_bar[threadIdx.x], 1);
   if (threadIdx.x == 0) mbar_init(h_bar, blockDim.x);
   fence_mbar_init();
+  if (w == 0) build_range_table(lo_tab, N, D, V);
   const int nw = lpc * LW;
   uint32_t cols = 32;
   while (cols < (uint32_t)(((nw + 3) / 4) * COLS)) cols <<= 1;
@@ -179,7 +206,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     tmem_st<ACC>(tbase + ACC, z);
   }
   const int total = D * N;
-  const int r0 = range_lo(v, N, D, V), r1 = range_lo(v + 1, N, D, V);
+#ifdef OFDMRX_BAL_EVEN_SPLIT
+  const int r0 = (int)((long long)total * v / V), r1 = (int)((long long)total * (v + 1) / V);  // experiment
+#else
+  const int r0 = lo_tab[v], r1 = lo_tab[v + 1];
+#endif
   int k = 0;  // stage counter across both phases
   if (leader && v < N) issue_rx(row_addr(0, v), 0);
   float2 y[P];
@@ -377,7 +408,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
       // add the partials of the following lanes that continue this symbol, in
       // lane order; lanes without rows are skipped (N < V leaves some empty)
       for (int q = v + 1; q < V; ++q) {
-        const int q0 = range_lo(q, N, D, V), q1 = range_lo(q + 1, N, D, V);
+#ifdef OFDMRX_BAL_EVEN_SPLIT
+        const int q0 = (int)((long long)total * q / V), q1 = (int)((long long)total * (q + 1) / V);
+#else
+        const int q0 = lo_tab[q], q1 = lo_tab[q + 1];
+#endif
         if (q0 >= q1) continue;
         if (q0 / N != d_own || q0 % N == 0) break;
         const uint32_t rk = (uint32_t)(q / lpc);
@@ -485,7 +520,7 @@ bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
   // SM count suggests, and the epilogue waits on every CTA of the frame).
   (void)n_ant;
   const int c = (n_data + 1 + LMAX - 1) / LMAX;
-  if (c > BMAX_CLUSTER) return false;
+  if (c > BMAX_CLUSTER || c * LMAX > BMAX_V) return false;
   const int V = c * LMAX;
   // CTA mapping depends on the batch: the fewest CTAs per frame (largest
   // lpc) that still give every SM a CTA, within the portable cluster size

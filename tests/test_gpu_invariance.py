@@ -26,7 +26,7 @@ SHAPES = [
     (256, 2048, 256, 64, 10, 2, (1, 2, 16, 64)),      # C4: balanced kernel, M = 2048 lanes of 64 threads
     (8, 64, 16, 4, 10, 3, (1, 2, 64, 4096)),          # C1: fused kernel
     (16, 256, 32, 16, 10, 3, (1, 2, 64, 1000)),       # C2: fused kernel
-    (4, 4096, 512, 16, 3, 2, (1, 3, 40)),             # M = 4096: lanes of 128 threads
+    (4, 4096, 512, 16, 3, 2, (1, 3, 100)),             # M = 4096: lanes of 128 threads
     (2, 1024, 72, 4, 5, 2, (1, 7, 300)),              # N < workers: lanes without rows
 ]
 
