@@ -26,6 +26,30 @@ def require_cuda(device=None):
     return dev
 
 
+class on_stream:
+    """Run allocations and launches of one call on `stream` (None = the
+    current stream).  The stream first waits for the current stream, so
+    inputs produced there are ready, and tensors allocated inside belong to
+    `stream` in the caching allocator (a scratch buffer freed on return is
+    only reused by later work on the same stream, never while a kernel on
+    `stream` may still touch it)."""
+
+    def __init__(self, stream):
+        self.stream = stream
+        self.ctx = None
+
+    def __enter__(self):
+        if self.stream is not None and self.stream != torch.cuda.current_stream(self.stream.device):
+            self.stream.wait_stream(torch.cuda.current_stream(self.stream.device))
+            self.ctx = torch.cuda.stream(self.stream)
+            self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+
+
 def stream_handle(stream=None):
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes_void(s.cuda_stream)

@@ -124,17 +124,14 @@ def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards=
     desc = device.make_desc(*desc_args, options=device.pilot_options(pvals), rx_samples=x.numel())
     device.check_desc(desc)
     pv = _PILOTS.get(pvals, x.device)
-    if out is None:
-        out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, x.device, want_h=want_h, zf=zf)
-    else:
-        if stream is not None:
-            with torch.cuda.stream(stream):
-                out.flags.zero_()
+    with device.on_stream(stream):  # outputs allocated / zeroed on the launch stream
+        if out is None:
+            out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, x.device, want_h=want_h, zf=zf)
         else:
             out.flags.zero_()
-    _lib.call("ofdmrx_rx_frames", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(out.H),
-              device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
-              device.ptr(out.flags), device.stream_handle(stream))
+        _lib.call("ofdmrx_rx_frames", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(out.H),
+                  device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
+                  device.ptr(out.flags), device.stream_handle(stream))
     if check:
         device.raise_on_flags(out.flags)
     return out
@@ -194,12 +191,13 @@ def receive_partials(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=
                             options=device.pilot_options(pvals), rx_samples=x.numel())
     device.check_desc(desc)
     pv = _PILOTS.get(pvals, dev)
-    H = torch.empty((f, n, cfg.fft_len), dtype=torch.complex64, device=dev) if want_h else None
-    num = torch.empty((f, n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
-    den = torch.empty((f, cfg.fft_len), dtype=torch.float32, device=dev)
-    flags = torch.zeros((f,), dtype=torch.int32, device=dev)
-    _lib.call("ofdmrx_rx_partials", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(H),
-              device.ptr(num), device.ptr(den), device.ptr(flags), device.stream_handle(stream))
+    with device.on_stream(stream):
+        H = torch.empty((f, n, cfg.fft_len), dtype=torch.complex64, device=dev) if want_h else None
+        num = torch.empty((f, n_data, cfg.fft_len), dtype=torch.complex64, device=dev)
+        den = torch.empty((f, cfg.fft_len), dtype=torch.float32, device=dev)
+        flags = torch.zeros((f,), dtype=torch.int32, device=dev)
+        _lib.call("ofdmrx_rx_partials", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(H),
+                  device.ptr(num), device.ptr(den), device.ptr(flags), device.stream_handle(stream))
     return H, num, den, flags
 
 
@@ -212,13 +210,15 @@ def finish_partials(num_parts, den_parts, qam_order, eps=device.MRC_WEIGHT_FLOOR
         raise ContractError(f"den partials {tuple(den_parts.shape)} do not match num {tuple(num_parts.shape)}")
     dev = num_parts.device
     qb = device.qam_bits(qam_order)
-    s_hat = torch.empty((f, d, m), dtype=torch.complex64, device=dev)
-    weights = torch.empty((f, m), dtype=torch.float32, device=dev)
-    bits = torch.empty((f, d * m * qb), dtype=torch.uint8, device=dev)
-    flags = torch.zeros((f,), dtype=torch.int32, device=dev)
-    _lib.call("ofdmrx_mrc_finish", f, d, m, int(qam_order), g, device.ptr(num_parts.contiguous()),
-              device.ptr(den_parts.contiguous()), float(eps), device.ptr(s_hat), device.ptr(weights),
-              device.ptr(bits), device.ptr(flags), device.stream_handle(stream))
+    with device.on_stream(stream):
+        nump, denp = num_parts.contiguous(), den_parts.contiguous()
+        s_hat = torch.empty((f, d, m), dtype=torch.complex64, device=dev)
+        weights = torch.empty((f, m), dtype=torch.float32, device=dev)
+        bits = torch.empty((f, d * m * qb), dtype=torch.uint8, device=dev)
+        flags = torch.zeros((f,), dtype=torch.int32, device=dev)
+        _lib.call("ofdmrx_mrc_finish", f, d, m, int(qam_order), g, device.ptr(nump), device.ptr(denp), float(eps),
+                  device.ptr(s_hat), device.ptr(weights), device.ptr(bits), device.ptr(flags),
+                  device.stream_handle(stream))
     return s_hat, weights, bits, flags
 
 
@@ -338,10 +338,10 @@ def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, ep
     desc = device.make_desc(f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, 0, s, n * s, eps,
                             options=device.pilot_options(pvals), rx_samples=x.numel())
     pv = _PILOTS.get(pvals, dev)
-    out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
-    _lib.call("ofdmrx_rx_frames_detected", ctypes.byref(desc), s, device.ptr(det.peak_index),
-              device.ptr(det.peak_metric), det.peak_index.shape[1], det.n_chips, thr, device.ptr(x), device.ptr(pv),
-              device.ptr(out.H),
-              device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
-              device.ptr(out.flags), device.stream_handle(stream))
+    with device.on_stream(stream):  # outputs zeroed on the stream the detection + receive run on
+        out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, dev, want_h=want_h, zf=zf)
+        _lib.call("ofdmrx_rx_frames_detected", ctypes.byref(desc), s, device.ptr(det.peak_index),
+                  device.ptr(det.peak_metric), det.peak_index.shape[1], det.n_chips, thr, device.ptr(x),
+                  device.ptr(pv), device.ptr(out.H), device.ptr(out.s_hat), device.ptr(out.weights),
+                  device.ptr(out.bits), device.ptr(out.zf), device.ptr(out.flags), device.stream_handle(stream))
     return out, det

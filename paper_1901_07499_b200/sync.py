@@ -130,13 +130,16 @@ def detect_frames(rx, pn, threshold=DEFAULT_THRESHOLD, *, antennas="all", scratc
     need = int(lib.ofdmrx_detect_scratch_bytes(f, n_rows, s, int(chips.size)))
     if need < 0:
         raise ContractError("invalid detection sizes")
-    if scratch is None or scratch.numel() < need:
-        scratch = torch.empty((max(need, 8),), dtype=torch.uint8, device=dev)
-    idx = torch.empty((f, n_rows), dtype=torch.int32, device=dev)
-    met = torch.empty((f, n_rows), dtype=torch.float64, device=dev)
     c = _CHIPS.get(chips, dev)
-    _lib.call("ofdmrx_detect", device.ptr(x), f, n_rows, s, s, n * s, device.ptr(c), int(chips.size),
-              device.ptr(scratch), device.ptr(idx), device.ptr(met), device.stream_handle(stream))
+    with device.on_stream(stream):  # scratch and outputs belong to the launch stream
+        if scratch is None or scratch.numel() < need:
+            scratch = torch.empty((max(need, 8),), dtype=torch.uint8, device=dev)
+        elif stream is not None:
+            scratch.record_stream(stream)
+        idx = torch.empty((f, n_rows), dtype=torch.int32, device=dev)
+        met = torch.empty((f, n_rows), dtype=torch.float64, device=dev)
+        _lib.call("ofdmrx_detect", device.ptr(x), f, n_rows, s, s, n * s, device.ptr(c), int(chips.size),
+                  device.ptr(scratch), device.ptr(idx), device.ptr(met), device.stream_handle(stream))
     return FrameDetections(peak_index=idx, peak_metric=met, n_chips=int(chips.size), threshold=float(threshold))
 
 
