@@ -145,6 +145,23 @@ OFDMRX_API int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, c
                      float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream);
 
 /*
+ * ofdmrx_rx_frames plus a per-stage attribution of the fused kernel's time,
+ * for StageTimings (receiver.py:65-79, 245-266) and per-stage µs/symbol of
+ * the fused path.  stage_cycles [F, 5] u64 (caller zeroes it) receives, per
+ * frame, the SM clock cycles all FFT lanes of the frame spent in
+ *   [0] pilot symbol: sample wait + FFT        (fft_s of the pilot slot)
+ *   [1] LS estimate H = Y conj(P), |H|^2       (combine_s of the pilot, "ls")
+ *   [2] data symbols: sample wait + FFT        (fft_s of the data slots)
+ *   [3] MRC accumulation conj(H) Y (+ ZF)      (combine_s of the data, "mrc")
+ *   [4] combine, divide, demap, stores         (combine_s of the data, "mrc")
+ * Shares of the sum apportion the measured kernel time; the results are the
+ * same as ofdmrx_rx_frames'.
+ */
+OFDMRX_API int ofdmrx_rx_frames_profiled(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H,
+                                         void* s_hat, float* weights, uint8_t* bits, void* zf, uint32_t* flags,
+                                         uint64_t* stage_cycles, void* stream);
+
+/*
  * ofdmrx_rx_frames with each frame's symbol0 taken from a device-side
  * detection (ofdmrx_detect outputs, no host round trip): symbol0 of frame f
  * = peak_index[f * peak_stride] + n_chips (DetectionResult.symbol0_offset,

@@ -100,6 +100,7 @@ SIGNATURES = {
     "ofdmrx_rx_plan": (ctypes.c_int, [_DESC, _i32, _i32, ctypes.POINTER(Plan)]),
     "ofdmrx_rx_frames": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "ofdmrx_rx_partials": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _p, _p]),
+    "ofdmrx_rx_frames_profiled": (ctypes.c_int, [_DESC, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "ofdmrx_mrc_finish": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _f32, _p, _p, _p, _p, _p]),
     "ofdmrx_fft_shift": (ctypes.c_int, [_DESC, _i32, _i32, _p, _p, _p]),
     "ofdmrx_ls": (ctypes.c_int, [_i32, _i32, _i32, _p, _i64, _p, _p, _p]),

@@ -162,7 +162,8 @@ int make_plan(const ofdmrx_frame_desc* d, RxPlan* pl) {
 
 int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, int mode, void* H, void* s_hat,
                  float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* num, float* den, void* stream,
-                 const Route* route = nullptr, const Detected* det = nullptr) {
+                 const Route* route = nullptr, const Detected* det = nullptr,
+                 unsigned long long* stage_cycles = nullptr) {
   if (int rc = check_desc_impl(d, det != nullptr ? det->n_samples : -1)) return rc;
   if (d->n_frames == 0) return OFDMRX_OK;
   if (int rc = check_ptr(rx, "rx")) return rc;
@@ -218,6 +219,7 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   p.flags = flags;
   p.part_num = static_cast<float2*>(num);
   p.part_den = den;
+  p.stage_cycles = stage_cycles;
   if (det != nullptr) {
     p.det_idx = det->idx;
     p.det_metric = det->metric;
@@ -391,6 +393,15 @@ int ofdmrx_rx_plan(const ofdmrx_frame_desc* desc, int32_t mode, int32_t zf, ofdm
 int ofdmrx_rx_frames(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
                      float* weights, uint8_t* bits, void* zf, uint32_t* flags, void* stream) {
   return fused_common(desc, rx, pilot, 0, H, s_hat, weights, bits, zf, flags, nullptr, nullptr, stream);
+}
+
+int ofdmrx_rx_frames_profiled(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* s_hat,
+                              float* weights, uint8_t* bits, void* zf, uint32_t* flags, uint64_t* stage_cycles,
+                              void* stream) {
+  if (desc != nullptr && desc->n_frames > 0)
+    if (int rc = check_ptr(stage_cycles, "stage_cycles")) return rc;
+  return fused_common(desc, rx, pilot, 0, H, s_hat, weights, bits, zf, flags, nullptr, nullptr, stream, nullptr,
+                      nullptr, reinterpret_cast<unsigned long long*>(stage_cycles));
 }
 
 int ofdmrx_rx_partials(const ofdmrx_frame_desc* desc, const void* rx, const void* pilot, void* H, void* num,

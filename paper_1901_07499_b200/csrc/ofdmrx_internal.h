@@ -63,7 +63,24 @@ struct FusedParams {
   int det_stride, det_add;
   double det_threshold;
   long long n_samples;
+  // optional per-stage attribution (ofdmrx_rx_frames_profiled): SM clock
+  // cycles of every lane, summed per frame and stage (kStage*)
+  unsigned long long* stage_cycles;  // [F, kStages]
 };
+
+// stages of the per-stage attribution (StageTimings fields, receiver.py:65-79)
+constexpr int kStagePilotFft = 0;  // pilot symbol: TMA wait + FFT          -> fft_s  (pilot)
+constexpr int kStageLs = 1;        // H = Y conj(P), |H|^2, H store          -> combine_s (pilot, "ls")
+constexpr int kStageDataFft = 2;   // data symbols: TMA wait + FFT          -> fft_s  (data)
+constexpr int kStageMrc = 3;       // conj(H) Y accumulation (+ ZF output)   -> combine_s (data, "mrc")
+constexpr int kStageDemap = 4;     // combine, divide, demap, stores         -> combine_s (data, "mrc")
+constexpr int kStages = 5;
+
+__device__ __forceinline__ uint32_t sm_clock() {
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
+  return c;
+}
 
 // per-frame symbol0 (detected or fixed) and the frame's admission flags
 __device__ __forceinline__ long long frame_sym0(const FusedParams& p, int f, int M, uint32_t* reject) {

@@ -128,7 +128,7 @@ __device__ __forceinline__ float2 ld_dsmem2(uint32_t a) {
   return v;
 }
 
-template <int M, bool BPSK, bool ZF>
+template <int M, bool BPSK, bool ZF, bool PROF>
 __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedParams p) {
   using BC = BalCfg<M>;
   constexpr int P = BC::P, G = BC::G, LW = BC::LW, SS = BC::SLOT, ACC = BC::ACC, COLS = BC::COLS;
@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   uint64_t* h_bar = rx_bar + 2 * BC::LPC_MAX;                 // H rows published (one-CTA frames)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_bar + 1);
   int* lo_tab = reinterpret_cast<int*>(smem_raw + 256);  // [V + 1]
+  uint32_t* cyc = reinterpret_cast<uint32_t*>(smem_raw + 768) + l * kStages;  // this lane's stage cycles
+  constexpr bool prof = PROF;  // per-stage attribution build (ofdmrx_rx_frames_profiled)
 #ifdef OFDMRX_BAL_CLUSTER_BAR
   const bool one_cta = false;  // experiment: the cluster barrier even for one-CTA frames
 #else
@@ -163,6 +165,10 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   };
 
   if (threadIdx.x < 2 * lpc) mbar_init(&rx_bar[threadIdx.x], 1);
+  if (prof && leader) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) cyc[s] = 0u;
+  }
   if (threadIdx.x == 0) mbar_init(h_bar, blockDim.x);
   fence_mbar_init();
   if (w == 0) build_range_table(lo_tab, N, D, V);
@@ -221,12 +227,18 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
       if (n + V < N) issue_rx(row_addr(0, n + V), st ^ 1);
       else if (r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), st ^ 1);  // first data row of phase B
     }
+    uint32_t tc = prof ? sm_clock() : 0u;
     wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(0, n)) >> 3) & 1);
     const float2* src = slot + sh;
     fft_forward<M>(y, slot, t, [&](int idx) { return src[idx]; }, lane_sync);
     fence_proxy_async_smem();
     lane_sync();
+    if (prof) {
+      const uint32_t t1 = sm_clock();
+      if (leader) cyc[kStagePilotFft] += t1 - tc;
+      tc = t1;
+    }
     float2* hdst = Hf + (long long)n * M + t;
     float dp[P];
     tmem_wait_st();
@@ -247,6 +259,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
       hdst[shifted_bin<M>(i, 0)] = h;
     }
     tmem_st<P>(t_den, dp);
+    if (prof && leader) cyc[kStageLs] += sm_clock() - tc;
   }
   if (leader && v >= N && r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), k & 1);  // no pilot rows
   tmem_wait_st();
@@ -274,6 +287,7 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     const int st = k & 1;
     float2* slot = slot_base + (size_t)st * SS;
     if (leader && r + 1 < r1) issue_rx(row_addr(1 + dn, nn), st ^ 1);
+    uint32_t tc = prof ? sm_clock() : 0u;
     wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(1 + d, n)) >> 3) & 1);
     const float2* src = slot + sh;
@@ -291,6 +305,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
       for (int i = 0; i < P; ++i) hreg[i] = __ldcg(hsrc + shifted_bin<M>(i, 0));
     });
     const uint32_t tacc = tbase + (uint32_t)((d - d_first) * ACC);
+    if (prof) {
+      const uint32_t t1 = sm_clock();
+      if (leader) cyc[kStageDataFft] += t1 - tc;
+      tc = t1;
+    }
     tmem_wait_st();
     // MAC in 16-column TMEM chunks: keeps y + hreg + one chunk in registers
     static_for<ACC / 16>([&](auto ci) {
@@ -321,12 +340,14 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     }
     fence_proxy_async_smem();  // reads of this slot before its next TMA refill
     lane_sync();
+    if (prof && leader) cyc[kStageMrc] += sm_clock() - tc;
     d = dn, n = nn;
     if (++nn == N) nn = 0, ++dn;
   }
   if (!h_acquired) h_acquire();
 
   // ---------------- epilogue -------------------------------------------------
+  const uint32_t t_epi = prof ? sm_clock() : 0u;
   // every lane parks its den partial (and the partial of a symbol it
   // continues) in the now idle TMA slots of its CTA; the cluster reads them
   tmem_wait_st();
@@ -463,6 +484,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     }
   }
   if (flag != 0u && p.flags != nullptr) atomicOr(&p.flags[f], flag);
+  if (prof && leader) {
+    cyc[kStageDemap] += sm_clock() - t_epi;
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) atomicAdd(&p.stage_cycles[(long long)f * kStages + s], (unsigned long long)cyc[s]);
+  }
   // remote readers of this CTA's partials are done before it exits
   tmem_fence_before();
   frame_sync();
@@ -471,11 +497,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   if (p.num_dst != nullptr && threadIdx.x == 0) __threadfence_system();  // peer stores before the exchange flags
 }
 
-template <int M, bool BPSK, bool ZF>
+template <int M, bool BPSK, bool ZF, bool PROF>
 cudaError_t launch_t(const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
   using BC = BalCfg<M>;
   static unsigned done = 0;
-  auto kern = rx_balanced_kernel<M, BPSK, ZF>;
+  auto kern = rx_balanced_kernel<M, BPSK, ZF, PROF>;
   if (cudaError_t e = ensure_smem_attr(kern, (int)BC::smem_bytes(BC::LPC_MAX), done); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.n_frames * (unsigned)bp.cluster, 1, 1);
@@ -502,11 +528,16 @@ cudaError_t launch_t(const FusedParams& p, const BalancedPlan& bp, cudaStream_t 
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
+template <int M, bool PROF>
+cudaError_t launch_mp(const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
+  const bool zf = p.zf != nullptr;
+  if (p.pilot_bpsk) return zf ? launch_t<M, true, true, PROF>(p, bp, s) : launch_t<M, true, false, PROF>(p, bp, s);
+  return zf ? launch_t<M, false, true, PROF>(p, bp, s) : launch_t<M, false, false, PROF>(p, bp, s);
+}
+
 template <int M>
 cudaError_t launch_m(const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
-  const bool zf = p.zf != nullptr;
-  if (p.pilot_bpsk) return zf ? launch_t<M, true, true>(p, bp, s) : launch_t<M, true, false>(p, bp, s);
-  return zf ? launch_t<M, false, true>(p, bp, s) : launch_t<M, false, false>(p, bp, s);
+  return p.stage_cycles != nullptr ? launch_mp<M, true>(p, bp, s) : launch_mp<M, false>(p, bp, s);
 }
 
 template <int M>

@@ -199,6 +199,8 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   }
 
   const bool write_h = is_pilot && active && chunk == 0 && p.H != nullptr;
+  const bool prof = p.stage_cycles != nullptr;
+  uint32_t c_fft = 0u, c_comb = 0u;  // this lane's stage cycles (per-stage attribution)
   float2 v[P];
   float2* hring_grp = ring + (size_t)grp * RING * GI * HS + (size_t)sub * HS;
 
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     const int st = NSTAGE == 2 ? (k & 1) : 0;
     if (kLoadEvery && NSTAGE == 2 && leader && n + n_step < p.n_ant) issue(n + n_step, st ^ 1);  // freed at the end of step k-1
     float2* slot = slots + (size_t)(st * lanes + lane) * SS;
+    uint32_t tc = prof ? sm_clock() : 0u;
     if (active && (kLoadEvery || k == 0)) mbar_wait_parity(&tma_bar[st * lanes + lane], NSTAGE == 2 ? ((k >> 1) & 1) : (k & 1));
     const int sh = (int)((reinterpret_cast<uintptr_t>(row0 + (long long)n * p.row_stride) >> 3) & 1);
     const float2* src = slot + sh;
@@ -218,6 +221,11 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     fence_proxy_async_smem();  // this thread's generic smem writes before the async-proxy refill
     unit_sync();               // every read of the slot done: it may be refilled
     if (kLoadEvery && NSTAGE == 1 && leader && n + n_step < p.n_ant) issue(n + n_step, 0);
+    if (prof) {
+      const uint32_t t1 = sm_clock();
+      c_fft += t1 - tc;
+      tc = t1;
+    }
 
     const int r = n % RING;
     const int j = n / RING;
@@ -287,7 +295,9 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
       if (u == 0) mbar_arrive(&empty_bar[grp * RING + r]);
       acc_store(a);
     }
+    if (prof) c_comb += sm_clock() - tc;
   }
+  const uint32_t t_epi = prof ? sm_clock() : 0u;
 
   // ---- epilogue: combine the pilots' den partials, divide, demap ----------
   float a[NACC];
@@ -370,6 +380,12 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     }
   }
   if (flag != 0u && p.flags != nullptr) atomicOr(&p.flags[f], flag);
+  if (prof && active && t == 0) {
+    unsigned long long* sc = p.stage_cycles + (long long)f * kStages;
+    atomicAdd(sc + (is_pilot ? kStagePilotFft : kStageDataFft), (unsigned long long)c_fft);
+    atomicAdd(sc + (is_pilot ? kStageLs : kStageMrc), (unsigned long long)c_comb);
+    atomicAdd(sc + kStageDemap, (unsigned long long)(sm_clock() - t_epi));
+  }
   if (p.num_dst != nullptr) __threadfence_system();  // peer stores before the exchange flags
 }
 

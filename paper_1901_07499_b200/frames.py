@@ -35,6 +35,17 @@ class FrameBatch:
     bits: torch.Tensor     # [F, D*M*b] uint8     PipelineResult.bits
     flags: torch.Tensor    # [F]       int32      OR of FLAG_NONFINITE / FLAG_ERASED
     zf: torch.Tensor = None  # [F, D, N, M] per-antenna ZF output (optional)
+    # [F, 5] int64 SM cycles per stage (pilot FFT, LS, data FFT, MRC, combine+demap),
+    # only with receive_frames(profile=True) (ofdmrx_rx_frames_profiled)
+    stage_cycles: torch.Tensor = None
+
+    def stage_shares(self):
+        """Fraction of the fused kernel's lane time per stage, summed over the
+        batch: (pilot_fft, ls, data_fft, mrc, combine_demap)."""
+        if self.stage_cycles is None:
+            raise ContractError("receive_frames(profile=True) records the stage cycles")
+        tot = self.stage_cycles.sum(0).double()
+        return (tot / max(float(tot.sum()), 1.0)).tolist()
 
     @property
     def erased(self):
@@ -45,10 +56,8 @@ class FrameBatch:
 def _pilot_values(pilot, fft_len):
     if pilot is None:
         pilot = make_pilot(fft_len)
-    if isinstance(pilot, PilotDefinition):
-        vals = pilot.values
-    else:
-        vals = pilot
+    # a PilotDefinition (ours or the reference's, waveform.py:204-211) or the values
+    vals = pilot.values if isinstance(pilot, PilotDefinition) or hasattr(pilot, "values") else pilot
     vals = np.asarray(vals.cpu() if isinstance(vals, torch.Tensor) else vals)
     if vals.shape != (fft_len,):
         raise ContractError(f"pilot has {vals.shape} values, config needs ({fft_len},)")
@@ -90,14 +99,16 @@ def allocate_outputs(n_frames, n_antennas, fft_len, n_data, qam_order, dev, want
 
 
 def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
-                   out=None, want_h=True, zf=False, check=False, stream=None, shards=None):
+                   out=None, want_h=True, zf=False, check=False, stream=None, shards=None, profile=False):
     """Fused receive of a batch of captures on the current CUDA device.
 
     rx: complex64 CUDA tensor [F, N, S] or [N, S] (numpy is copied H2D).
     Returns a FrameBatch.  With check=True, raises NumericInputError when a
     frame fed non-finite samples to the FFT (forces a device sync).  Results
     do not depend on the batch (F) a frame is received in; `shards` is
-    accepted for compatibility and ignored."""
+    accepted for compatibility and ignored.  profile=True also records the
+    per-stage SM cycles of the fused kernel (FrameBatch.stage_cycles; same
+    results, an instrumented build of the kernel)."""
     if not isinstance(cfg, OfdmConfig):
         raise ContractError("cfg must be an OfdmConfig")
     dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
@@ -115,10 +126,10 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     if n_data < 0 or symbol0_offset < 0:
         raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
     desc_args = (f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
-    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream)
+    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=profile)
 
 
-def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards=None):
+def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=False):
     f, n, _, _, n_data = desc_args[:5]
     pvals = _pilot_values(pilot, cfg.fft_len)
     desc = device.make_desc(*desc_args, options=device.pilot_options(pvals), rx_samples=x.numel())
@@ -129,9 +140,16 @@ def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, shards=
             out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, x.device, want_h=want_h, zf=zf)
         else:
             out.flags.zero_()
-        _lib.call("ofdmrx_rx_frames", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(out.H),
-                  device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
-                  device.ptr(out.flags), device.stream_handle(stream))
+        if profile:
+            out.stage_cycles = torch.zeros((f, 5), dtype=torch.int64, device=x.device)
+            _lib.call("ofdmrx_rx_frames_profiled", ctypes.byref(desc), device.ptr(x), device.ptr(pv),
+                      device.ptr(out.H), device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits),
+                      device.ptr(out.zf), device.ptr(out.flags), device.ptr(out.stage_cycles),
+                      device.stream_handle(stream))
+        else:
+            _lib.call("ofdmrx_rx_frames", ctypes.byref(desc), device.ptr(x), device.ptr(pv), device.ptr(out.H),
+                      device.ptr(out.s_hat), device.ptr(out.weights), device.ptr(out.bits), device.ptr(out.zf),
+                      device.ptr(out.flags), device.stream_handle(stream))
     if check:
         device.raise_on_flags(out.flags)
     return out

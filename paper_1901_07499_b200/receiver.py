@@ -112,9 +112,14 @@ class B200Engine:
 
     ``tree`` selects the antenna-sum order: False = ascending (mrc_seq),
     True = the reference pairwise tree (mrc_tree).  ``fused`` makes
-    run_ring_pipeline use the single fused kernel per frame."""
+    run_ring_pipeline use the single fused kernel per pilot-led segment.
+    The reference's own run_ring_pipeline / process_symbol drive it through
+    freq_transform / ls_divide / mrc like any reference engine
+    (tests/test_gpu_reference_dropin.py)."""
 
     def __init__(self, variant="b200", worker_count=1, tree=False, fused=True, device_index=None):
+        if worker_count < 1:
+            raise ConfigurationError("worker_count must be >= 1")
         self.variant = variant
         self.worker_count = worker_count
         self.tree = tree
@@ -145,13 +150,37 @@ class B200Engine:
         self.close()
 
 
-SequentialEngine = B200Engine  # name kept for drop-in imports
+class SequentialEngine(B200Engine):
+    """receiver.py:88-108 on the device.  Per-symbol calls (process_symbol)
+    sum antennas in ascending order (mrc_seq); run_ring_pipeline batches each
+    pilot-led segment into one fused launch (see ofdmrx_rx_plan for its
+    antenna-sum order)."""
+
+    def __init__(self, device_index=None):
+        super().__init__(variant="sequential", worker_count=1, tree=False, fused=True, device_index=device_index)
+
+
+class DataParallelEngine(B200Engine):
+    """receiver.py:111-173 on the device: the reference fans the per-antenna
+    FFTs and per-subcarrier LS / MRC chunks over a worker pool; here the same
+    decomposition is the kernels' grid (one FFT lane per antenna row, one
+    thread per subcarrier), so ``worker_count`` only mirrors the attribute.
+    Antenna sums follow the reference pairwise tree (mrc_tree,
+    numerics.ReductionPlan), so results do not depend on worker_count, as in
+    the reference.  close() is a no-op (no pool)."""
+
+    def __init__(self, worker_count=4, device_index=None):
+        super().__init__(variant="data_parallel", worker_count=worker_count, tree=True, fused=False,
+                         device_index=device_index)
 
 
 def make_engine(kind):
     """receiver.py:176-179: every variant runs on the B200."""
-    tree = kind.variant == "data_parallel"
-    return B200Engine(variant=kind.variant, worker_count=kind.worker_count, tree=tree, fused=not tree)
+    if kind.variant == "sequential":
+        return SequentialEngine()
+    if kind.variant == "data_parallel":
+        return DataParallelEngine(kind.worker_count)
+    return B200Engine(variant=kind.variant, worker_count=kind.worker_count, tree=False, fused=True)
 
 
 # ---------------------------------------------------------------------------
@@ -280,37 +309,66 @@ def _segments(slots):
 
 
 def _run_fused(slots, cfg, engine, pilot):
+    """Each pilot-led segment is one fused launch; StageTimings per slot keep
+    the reference's meaning (receiver.py:65-79, 245-266, 330-332):
+      read_s     getting the slot's samples onto the device: host staging of
+                 the segment plus its H2D copy (CUDA events), split by bytes;
+      cp_drop_s  the host-side cp_drop / framing and finiteness checks;
+      fft_s      the fused kernel's time in the slot's FFT (incl. sample wait);
+      combine_s  ls (pilot) or mrc + demap (data), and the D2H of the results.
+    The kernel's time is apportioned by ofdmrx_rx_frames_profiled's per-stage
+    SM cycles (pilot FFT / LS / data FFT / MRC / combine+demap)."""
     pilot = pilot or waveform.make_pilot(cfg.fft_len)
     estimate, symbols, timings = None, [], []
     for seg in _segments(slots):
+        n_sym = len(seg)
+        t0 = time.perf_counter()
         for s in seg:
             if np.atleast_2d(s.payload).shape[1] != cfg.symbol_len:
                 raise FramingError(
                     f"symbol rows have {np.atleast_2d(s.payload).shape[1]} samples, expected {cfg.symbol_len}")
-        t0 = time.perf_counter()
-        capture = np.concatenate([np.atleast_2d(s.payload) for s in seg], axis=1)
-        if not np.all(np.isfinite(capture[:, np.arange(capture.shape[1]) % cfg.symbol_len >= cfg.cp_len])):
-            raise NumericInputError("non-finite samples entering the FFT stage")
+        payload = [np.atleast_2d(s.payload) for s in seg]
+        for p in payload:
+            if not np.all(np.isfinite(p[:, cfg.cp_len:])):
+                raise NumericInputError("non-finite samples entering the FFT stage")
+        t1 = time.perf_counter()
+        capture = np.ascontiguousarray(np.concatenate(payload, axis=1), dtype=np.complex64)
         with torch.cuda.device(engine.device):
-            x = device.as_c64(capture, engine.device)
-            t1 = time.perf_counter()
-            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            start.record()
-            out = frames.receive_frames(x, cfg, pilot, n_data=len(seg) - 1)
-            stop.record()
-            H = _to_host_c128(out.H[0])
-            s_hat = _to_host_c128(out.s_hat[0])
-            w = out.weights[0].cpu().numpy().astype(np.float64)
-            bits = out.bits[0].cpu().numpy()
-            kernel_s = start.elapsed_time(stop) * 1e-3
-        per = kernel_s / len(seg)
+            host = torch.from_numpy(capture).pin_memory()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            t2 = time.perf_counter()
+            ev[0].record()
+            x = host.to(engine.device, non_blocking=True)
+            ev[1].record()
+            out = frames.receive_frames(x, cfg, pilot, n_data=n_sym - 1, profile=True)
+            ev[2].record()
+            H = out.H[0].cpu()
+            ev[3].record()
+            s_hat, w, bits = out.s_hat[0].cpu(), out.weights[0].cpu(), out.bits[0].cpu()
+            ev[4].record()
+            shares = out.stage_shares()
+            torch.cuda.synchronize()
+            h2d_s = ev[0].elapsed_time(ev[1]) * 1e-3
+            kernel_s = ev[1].elapsed_time(ev[2]) * 1e-3
+            d2h_h_s = ev[2].elapsed_time(ev[3]) * 1e-3
+            d2h_s = ev[3].elapsed_time(ev[4]) * 1e-3
+        staging_s = t2 - t1
+        read = (staging_s + h2d_s) / n_sym
+        cp = (t1 - t0) / n_sym
+        H = H.numpy().astype(np.complex128)
+        s_hat = s_hat.numpy().astype(np.complex128)
+        w = w.numpy().astype(np.float64)
+        bits = bits.numpy()
         estimate = ChannelEstimate(gains=H, source_seq=seg[0].seq_no)
-        timings.append(StageTimings(kind=PILOT, read_s=t1 - t0, fft_s=per))
+        timings.append(StageTimings(kind=PILOT, read_s=read, cp_drop_s=cp, fft_s=kernel_s * shares[0],
+                                    combine_s=kernel_s * shares[1] + d2h_h_s))
         nb = cfg.fft_len * cfg.bits_per_qam_symbol
+        n_data = n_sym - 1
         for i, slot in enumerate(seg[1:]):
             symbols.append(CombinedSymbol(equalized=s_hat[i], seq_no=slot.seq_no, weight_norm=w.copy(),
                                           bits=bits[i * nb:(i + 1) * nb], erased=w < MRC_WEIGHT_FLOOR))
-            timings.append(StageTimings(kind=DATA, fft_s=per))
+            timings.append(StageTimings(kind=DATA, read_s=read, cp_drop_s=cp, fft_s=kernel_s * shares[2] / n_data,
+                                        combine_s=(kernel_s * (shares[3] + shares[4]) + d2h_s) / n_data))
     if estimate is None:
         raise PipelineOrderError("stream ended without a pilot symbol")
     return PipelineResult(estimate=estimate, symbols=symbols, timings=timings)
@@ -318,9 +376,9 @@ def _run_fused(slots, cfg, engine, pilot):
 
 def run_ring_pipeline(slots, cfg, engine, pilot=None, ring_capacity=64):
     """receiver.py:308-348.  With a fused engine each pilot-led segment is one
-    fused kernel launch (timings: H2D staging reported as read_s, kernel time
-    split evenly over the segment's symbols as fft_s); otherwise the slots go
-    through process_symbol one by one with per-stage timings."""
+    fused kernel launch (per-stage timings from the kernel's own stage
+    attribution, see _run_fused); otherwise the slots go through
+    process_symbol one by one with wall-clock per-stage timings."""
     if ring_capacity < 1 or (ring_capacity & (ring_capacity - 1)) != 0:
         raise ConfigurationError(f"ring capacity must be a power of two, got {ring_capacity}")
     slots = list(slots)
