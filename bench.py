@@ -44,6 +44,21 @@ def frame_bytes(n, m, qam, d):
     return 8 * n * m * (1 + d) + 8 * n * m + 8 * m * d + b * m * d
 
 
+KERNEL_SOURCES = ("rx_balanced.cu", "rx_fused.cu", "ofdmrx_fft.cuh", "ofdmrx_internal.h", "capi.cu")
+
+
+def kernel_source_hash():
+    """Hash of the receive kernels' sources: profiles/traffic_<cfg>.json
+    records it, so a capture taken on another kernel version reads as stale."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for name in KERNEL_SOURCES:
+        with open(os.path.join(ROOT, "paper_1901_07499_b200", "csrc", name), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -156,6 +171,11 @@ def dist_setup(n_gpus):
 
         torch.cuda.set_device(dev)
         if backend == "nccl":
+            # NCCL's init log (ranks, transports) into a file, not stdout: the
+            # JSON line stays the only stdout line; comm_info() quotes it
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/ofdmrx_nccl.{rank}.%p.log")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
@@ -415,6 +435,7 @@ def run_b200(args, cfg_name, world, rank, local):
     ber = float((out.bits[lo:hi].cpu().numpy() != bits_truth[idx % len(bits_truth)]).mean())
     flags_bad = int((out.flags != 0).sum())
     torch.cuda.synchronize()
+    oracle_check = check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, args.oracle_frames) if args.oracle_frames else None
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
@@ -436,9 +457,26 @@ def run_b200(args, cfg_name, world, rank, local):
             ev[i][1].record(stream)
         t_stop.record(stream)
         torch.cuda.synchronize()
-        clocks.mark(h0, time.time())
-        time.sleep(0.25)  # let nvidia-smi deliver the samples it took inside the window
+        h1 = time.time()
+        sustained = None
+        if args.sustained_steps > 0:
+            # a second, longer timed region right after the burst: the board's
+            # power cap engages after ~100 ms of back-to-back launches
+            barrier(world)
+            torch.cuda.synchronize()
+            s_start, s_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h2 = time.time()
+            s_start.record(stream)
+            for _ in range(args.sustained_steps):
+                step()
+            s_stop.record(stream)
+            torch.cuda.synchronize()
+            h3 = time.time()
+            sustained = (s_start.elapsed_time(s_stop), h2, h3)
+        time.sleep(0.25)  # let nvidia-smi deliver the samples it took inside the windows
         barrier(world)
+    clocks.mark(h0, h1)
+    burst_clocks = clocks.summary()
     total_ms = t_start.elapsed_time(t_stop)
     kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     ms_step = allreduce_max(world, total_ms / args.steps)
@@ -454,14 +492,19 @@ def run_b200(args, cfg_name, world, rank, local):
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
-        if "dram_bytes_per_frame" in tj:
+        fresh = tj.get("kernel_source_hash") == kernel_source_hash()
+        if "dram_bytes_per_frame" in tj and fresh:
             # same units as `achieved`: the ncu-measured DRAM bytes of one launch
-            # of this size over the live kernel time
+            # of this size over the live kernel time (only when the capture was
+            # taken on the kernel sources being measured)
             traffic = tj["dram_bytes_per_frame"] * F / (kernel_ms * 1e-3) / 1e9
             traffic_detail = {"dram_bytes_per_launch": int(tj["dram_bytes_per_frame"] * F),
                               "algorithmic_bytes_per_launch": int(frame_bytes(n // (world if sharded is not None else 1),
                                                                               m, qam, d) * F),
-                              "source": tj.get("source")}
+                              "source": tj.get("source"), "kernel_source_hash": tj.get("kernel_source_hash")}
+        elif "dram_bytes_per_frame" in tj:
+            traffic_detail = {"stale": f"{tj.get('source')} was captured on other kernel sources "
+                                       f"({tj.get('kernel_source_hash')} != {kernel_source_hash()})"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
@@ -479,10 +522,24 @@ def run_b200(args, cfg_name, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_detail": traffic_detail, "peak_source": peak_kind,
                      "bytes_per_frame": bpf, "kernel_ms": kernel_ms},
-        "clocks": clocks.summary(),
-        "check": {"ber_vs_tx": ber, "flagged_frames": flags_bad},
+        "clocks": burst_clocks,
+        "check": {"ber_vs_tx": ber, "flagged_frames": flags_bad, **(oracle_check or {})},
         "data_symbols_per_s": world * F * d / (ms_step * 1e-3),
     }
+    if sustained is not None:
+        clocks.mark(sustained[1], sustained[2])
+        s_ms = allreduce_max(world, sustained[0] / args.sustained_steps)
+        s_val = (1 if sharded is not None else world) * F * (1 + d) / (s_ms * 1e-3)
+        line["sustained"] = {"steps": args.sustained_steps, "ms_per_step": s_ms, "value": s_val,
+                             "roofline_frac": bpf * F / (s_ms * 1e-3) / 1e9 / peak, "clocks": clocks.summary(),
+                             "note": "same launches back to back for ~{:.0f} ms right after the burst; the headline "
+                                     "value is the {}-step burst".format(sustained[0], args.steps)}
+    if world > 1:
+        line["clocks_per_rank"] = gather_objects(world, {"rank": rank, "device": local, **burst_clocks})
+        line["check_per_rank"] = gather_objects(world, {"rank": rank, "frames": [lo, hi], "ber_vs_tx": ber,
+                                                        "flagged_frames": flags_bad, **(oracle_check or {})})
+        line["comm"] = comm_info(world, "none (frame sharding)" if sharded is None else
+                                  f"{args.exchange} exchange of the MRC partial sums")
     if args.e2e_frames > 0:
         line["e2e"] = run_e2e(args, cfg, x, s0, d, world)
     if not args.no_stages and world == 1 and cfg_name != "C4":
@@ -490,10 +547,166 @@ def run_b200(args, cfg_name, world, rank, local):
             line["stages"] = run_stages(args, cfg, x, s0, d)
         except Exception as exc:  # noqa: BLE001
             line["stages"] = {"error": repr(exc)[:300]}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if world == 1 and args.sweep_cells and cfg_name != "C4":
+        try:  # compact C5 sweep in the default line (full sweep: --sweep)
+            cells = [tuple(int(v) for v in c.split("x")) for c in args.sweep_cells.split(",")]
+            line["sweep"] = sweep_cells(cells, reps=1)[1]
+        except Exception as exc:  # noqa: BLE001
+            line["sweep"] = {"error": repr(exc)[:300]}
+    if world == 1 and args.latency and cfg_name != "C4":
+        try:
+            line["latency"] = run_latency(args)
+        except Exception as exc:  # noqa: BLE001
+            line["latency"] = {"error": repr(exc)[:300]}
+    if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = (cpu_reference_numpy_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds)
                                 or cpu_port_baseline(cfg_name, rx_host[:4], budget_s=args.cpu_seconds))
     return line
+
+
+def check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, max_frames):
+    """Parity of the benchmarked launch: the distinct frames' bits against the
+    CPU oracle (oracle/ofdm_oracle.py, the numpy restatement of the reference
+    pinned to reference-generated golden vectors), s_hat / H / weights within
+    north_star's 1e-4.  A checker outside the timed region, never measured."""
+    from oracle import ofdm_oracle as orc
+
+    n, m, cp, qam, d, _ = CONFIGS[cfg_name]
+    k = min(hi - lo, max_frames)
+    mism, worst = 0, {"s_hat": 0.0, "H": 0.0, "weights": 0.0}
+    bits_dev = out.bits[lo:lo + k].cpu().numpy()
+    sh_dev = out.s_hat[lo:lo + k].cpu().numpy()
+    w_dev = out.weights[lo:lo + k].cpu().numpy()
+    h_dev = out.H[lo:lo + k].cpu().numpy() if getattr(out, "H", None) is not None and out.H.shape[1] == n else None
+
+    def rel(a, b):
+        return float(np.linalg.norm(np.asarray(a, np.complex128) - b) / max(np.linalg.norm(b), 1e-300))
+
+    for i in range(k):
+        H, s_hat, w, bits = orc.receive_frame(rx_host[(lo + i) % len(rx_host)].astype(np.complex128), s0, m, cp, d, qam)
+        mism += int((bits_dev[i] != bits).sum())
+        worst["s_hat"] = max(worst["s_hat"], rel(sh_dev[i], s_hat))
+        worst["weights"] = max(worst["weights"], rel(w_dev[i], w))
+        if h_dev is not None:
+            worst["H"] = max(worst["H"], rel(h_dev[i], H))
+    return {"bits_vs_oracle": "exact" if mism == 0 else f"{mism} bits differ",
+            "oracle_frames": k, "oracle_bits": int(k * bits_dev.shape[1]),
+            "max_rel_err": worst, "rel_tol": 1e-4,
+            "oracle_ok": mism == 0 and max(worst.values()) < 1e-4,
+            "checker": "oracle/ofdm_oracle.py receive_frame (fp64 numpy restatement of the reference path), "
+                       "outside the timed region"}
+
+
+def gather_objects(world, obj):
+    import torch.distributed as dist
+
+    objs = [None] * world
+    dist.all_gather_object(objs, obj)
+    return objs
+
+
+def comm_info(world, data_path):
+    import torch
+    import torch.distributed as dist
+
+    info = {"backend": dist.get_backend(), "world_size": dist.get_world_size()}
+    if info["backend"] == "nccl":
+        v = torch.cuda.nccl.version()
+        info["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    info["data_path_collective"] = data_path
+    import glob
+
+    rank = dist.get_rank()
+    for path in sorted(glob.glob(f"/tmp/ofdmrx_nccl.{rank}.{os.getpid()}.log")):
+        with open(path, errors="replace") as fh:
+            keep = [ln.strip()[-160:] for ln in fh if "nranks" in ln or "Init COMPLETE" in ln or "NVLS" in ln]
+        info["nccl_init_log"] = keep[:4]
+    return info
+
+
+def run_latency(args):
+    """The paper's regime: ONE frame, pinned host capture
+    -> device -> fused receive -> bits back on the host, per call.  Reported
+    per config (C1, C3): the public-API call's wall time (median / p99 over
+    `latency_reps` calls, host-timed around H2D + kernel + D2H + sync), the
+    same sequence replayed as a CUDA graph (no Python), the kernel alone
+    (CUDA events) and its per-stage split from the kernel's own stage
+    attribution (ofdmrx_rx_frames_profiled), all per OFDM symbol."""
+    import torch
+
+    from paper_1901_07499_b200 import frames
+
+    res = {}
+    for name in ("C1", "C3"):
+        n, m, cp, qam, d, _ = CONFIGS[name]
+        cfg, rx_host, _, s0 = make_inputs(name)
+        host = torch.from_numpy(rx_host[:1]).pin_memory()
+        dev_x = torch.empty(host.shape, dtype=host.dtype, device="cuda")
+        out = frames.allocate_outputs(1, n, m, d, qam, dev_x.device)
+        bits_host = torch.empty(out.bits.shape, dtype=torch.uint8, pin_memory=True)
+
+        def call():
+            dev_x.copy_(host, non_blocking=True)
+            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
+            bits_host.copy_(out.bits, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(20):
+            call()
+        ts = []
+        for _ in range(args.latency_reps):
+            t0 = time.perf_counter()
+            call()
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        # same sequence as one CUDA graph (copy in, kernel, copy out)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                dev_x.copy_(host, non_blocking=True)
+                frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
+                bits_host.copy_(out.bits, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            dev_x.copy_(host, non_blocking=True)
+            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
+            bits_host.copy_(out.bits, non_blocking=True)
+        gts = []
+        for _ in range(args.latency_reps):
+            t0 = time.perf_counter()
+            g.replay()
+            torch.cuda.current_stream().synchronize()
+            gts.append(time.perf_counter() - t0)
+        gts.sort()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(50):
+            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
+        b.record()
+        torch.cuda.synchronize()
+        k_us = a.elapsed_time(b) / 50 * 1e3
+        prof = frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, profile=True)
+        torch.cuda.synchronize()
+        shares = prof.stage_shares()
+        sym = 1 + d
+        med, p99 = ts[len(ts) // 2] * 1e6, ts[min(len(ts) - 1, int(len(ts) * 0.99))] * 1e6
+        gmed = gts[len(gts) // 2] * 1e6
+        res[name] = {
+            "frames": 1, "symbols_per_frame": sym,
+            "h2d_bytes": int(host.numel() * 8), "d2h_bytes": int(bits_host.numel()),
+            "api_us_per_frame": {"median": med, "p99": p99}, "api_us_per_symbol": med / sym,
+            "graph_us_per_frame": gmed, "graph_us_per_symbol": gmed / sym,
+            "kernel_us_per_frame": k_us, "kernel_us_per_symbol": k_us / sym,
+            "kernel_stage_us_per_symbol": {
+                "fft": k_us * (shares[0] + shares[2]) / sym, "ls": k_us * shares[1],
+                "mrc": k_us * shares[3] / max(d, 1), "combine_demap": k_us * shares[4] / max(d, 1)},
+            "path": "pinned host [N, S] capture -> copy_ H2D -> frames.receive_frames (one fused launch) -> bits D2H "
+                    "-> stream sync; host perf_counter around each call"}
+        del dev_x, out
+    return res
 
 
 def run_e2e(args, cfg, x_dev, s0, d, world):
@@ -528,6 +741,7 @@ def run_e2e(args, cfg, x_dev, s0, d, world):
             "h2d_bytes_per_step": int(Fe * cfg.n_antennas * (1 + d) * cfg.fft_len * 8),
             "d2h_bytes_per_step": int(bits_host.numel()),
             "frames_per_step": Fe, "ms_per_step": ms, "chunk_frames": min(args.e2e_chunk, Fe),
+            "d2h": "bits only (PipelineResult.bits); s_hat / H / weights stay in HBM",
             "path": "pinned host cf32 captures -> frames.StreamingReceiver (ofdmrx_stage_symbols strided H2D of the "
                     "FFT windows only, CP never crosses PCIe | fused kernel | D2H bits, on 3 streams) "
                     "-> pinned host bits; host-timed around whole steps (includes sync)"}
@@ -660,89 +874,111 @@ def run_sync_stage(cfg, d, Fs, timed):
 # written in the reference bench CSV schema (ofdmrx/bench.py:22-24)
 # ---------------------------------------------------------------------------
 
-CSV_HEADER = "fft_len,cp_len,n_antennas,engine,workers,phase,stage,mean_us,std_us,n_symbols"
+def sweep_cells(cells, with_cpu=True, reps=3, max_frames=4096):
+    """C5 sweep cells (N antennas, FFT M): per-stage timing on the B200 next
+    to the reference CPU path, in the reference bench CSV schema
+    (ofdmrx/bench.py:19-25; paper_1901_07499_b200.benchcsv).
+
+    Per cell, on the same reference-built slots of one frame:
+      engine "sequential"  the unmodified reference run_ring_pipeline with its
+                           SequentialEngine (numba backend), records made by
+                           the reference's own _records_for_engine;
+      engine "b200"        the mirror's run_ring_pipeline (one fused launch,
+                           StageTimings with the reference's meaning: the
+                           paper's per-symbol regime incl. H2D/D2H);
+      engine "b200_batched" the staged kernels over F frames resident in HBM
+                           (GPU time per symbol: fft, ls, mrc = MRC + demap).
+    Plus, per cell, the fused kernel's time at batch F and its HBM roofline
+    fraction.  Returns (records, summary)."""
+    import torch
+
+    from paper_1901_07499_b200 import benchcsv, synth
+    from paper_1901_07499_b200 import receiver as mr
+    from paper_1901_07499_b200.waveform import OfdmConfig, default_cp
+
+    qam, d = 16, 10
+    ref = with_cpu and reference_importable()
+    if ref:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ofdmrx_numba_cache")
+        from ofdmrx import bench as bref, receiver as rref, waveform as wref
+        from ofdmrx.sync import DetectionResult
+    peak, _ = load_peaks()
+    records, summary = [], []
+    for n, m in cells:
+        cp = default_cp(m)
+        cfg = OfdmConfig(m, cp, n, qam_order=qam)
+        rx, _, s0 = synth.synth_batch(cfg, d, range(2), snr_db=10.0)
+        F = max(2, min(max_frames, (1 << 26) // (n * m * (1 + d))))
+        x = torch.from_numpy(rx).cuda().repeat((F + 1) // 2, 1, 1)[:F].contiguous()
+        st = run_stages(argparse.Namespace(stage_frames=F), cfg, x, s0, d, with_sync=False)
+        bpf = frame_bytes(n, m, qam, d)
+        fused_frame_us = st["fused_us_per_symbol"] * (1 + d)
+        frac = bpf / (fused_frame_us * 1e-6) / 1e9 / peak
+        for phase, stage, us, ns in (("estimation", "fft", st["fft_us_per_symbol"], F),
+                                     ("estimation", "ls", st["ls_us_per_pilot_symbol"], F),
+                                     ("demodulation", "fft", st["fft_us_per_symbol"], F * d),
+                                     ("demodulation", "mrc",
+                                      st["mrc_us_per_data_symbol"] + st["demap_us_per_data_symbol"], F * d)):
+            records.append(benchcsv.BenchRecord(m, cp, n, "b200_batched", 1, phase, stage, us, 0.0, ns))
+        cell = {"fft_len": m, "n_antennas": n, "frames": F, "fused_us_per_symbol": st["fused_us_per_symbol"],
+                "roofline_frac": frac, "bytes_per_frame": bpf,
+                "b200_batched_us_per_symbol": {"fft": st["fft_us_per_symbol"], "ls": st["ls_us_per_pilot_symbol"],
+                                               "mrc+demap": st["mrc_us_per_data_symbol"]
+                                               + st["demap_us_per_data_symbol"]}}
+        del x
+        torch.cuda.empty_cache()
+        if ref:
+            rcfg = wref.OfdmConfig(m, cp, n, qam_order=qam)
+            pilot = wref.make_pilot(m)
+
+            class _Cap:
+                def __init__(self, s):
+                    self.streams = s
+
+            slots = rref.extract_slots(_Cap(rx[0].astype(np.complex128)), DetectionResult(True, 0, s0, 1.0, ()),
+                                       rcfg, 1 + d)
+            with rref.make_engine(rref.EngineKind("sequential")) as eng:
+                warm = rref.run_ring_pipeline(slots, rcfg, eng, pilot=pilot)
+                timed = []
+                for _ in range(reps):
+                    res = rref.run_ring_pipeline(slots, rcfg, eng, pilot=pilot)
+                    timed.extend(res.timings)
+            records.extend(benchcsv.BenchRecord(**vars(r)) for r in
+                           bref._records_for_engine(rcfg, "sequential", 1, timed, warm.timings))
+            eng = mr.make_engine(mr.EngineKind("b200"))
+            warm_b = mr.run_ring_pipeline(slots, rcfg, eng, pilot=pilot)
+            timed_b = []
+            same = np.array_equal(warm_b.bits, warm.bits)
+            for _ in range(reps):
+                res_b = mr.run_ring_pipeline(slots, rcfg, eng, pilot=pilot)
+                same = same and np.array_equal(res_b.bits, warm.bits)
+                timed_b.extend(res_b.timings)
+            records.extend(benchcsv.records_for_engine(rcfg, "b200", 1, timed_b, warm_b.timings))
+            cell["bits_equal_reference"] = bool(same)
+            per = lambda ts: sum(t.total_s for t in ts) / len(ts) * 1e6  # noqa: E731
+            cell["pipeline_us_per_symbol"] = {"reference_sequential": per(timed), "b200": per(timed_b)}
+        summary.append(cell)
+        print(json.dumps(cell), file=sys.stderr, flush=True)
+    return records, summary
 
 
 def run_sweep(args):
-    import csv
-
     import torch
 
-    from paper_1901_07499_b200 import synth
-    from paper_1901_07499_b200.waveform import OfdmConfig, default_cp
+    from paper_1901_07499_b200 import benchcsv
 
     torch.cuda.set_device(0)
     ants = [int(a) for a in args.sweep_antennas.split(",")]
     ffts = [int(m) for m in args.sweep_ffts.split(",")]
-    qam, d = 16, 10
-    ref = reference_importable()
-    if ref:
-        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ofdmrx_numba_cache")
-        from ofdmrx import receiver as rref, waveform as wref
-    rows = []
-    summary = []
-    for m in ffts:
-        cp = default_cp(m)
-        for n in ants:
-            cfg = OfdmConfig(m, cp, n, qam_order=qam)
-            rx, _, s0 = synth.synth_batch(cfg, d, range(2), snr_db=10.0)
-            F = max(2, min(4096, (1 << 26) // (n * m * (1 + d))))
-            x = torch.from_numpy(rx).cuda().repeat((F + 1) // 2, 1, 1)[:F].contiguous()
-            st = run_stages(argparse.Namespace(stage_frames=F), cfg, x, s0, d, with_sync=False)
-            g = [("estimation", "fft", st["fft_us_per_symbol"], F),
-                 ("estimation", "ls", st["ls_us_per_pilot_symbol"], F),
-                 ("demodulation", "fft", st["fft_us_per_symbol"], F * d),
-                 ("demodulation", "mrc", st["mrc_us_per_data_symbol"] + st["demap_us_per_data_symbol"], F * d),
-                 ("demodulation", "fused", st["fused_us_per_symbol"], F * (1 + d))]
-            for phase, stage, us, ns in g:
-                rows.append((m, cp, n, "b200", 1, phase, stage, us, 0.0, ns))
-            cpu = {}
-            if ref:
-                rcfg = wref.OfdmConfig(m, cp, n, qam_order=qam)
-                pilot = wref.make_pilot(m)
-                eng = rref.SequentialEngine()
-                x0 = rx[0].astype(np.complex128)
-                sym = lambda k: x0[:, s0 + k * (m + cp): s0 + (k + 1) * (m + cp)]  # noqa: E731
-
-                def best(fn, reps=3):
-                    ts = []
-                    for _ in range(reps):
-                        t0 = time.perf_counter()
-                        out = fn()
-                        ts.append(time.perf_counter() - t0)
-                    return min(ts) * 1e6, out
-
-                best(lambda: rref.to_freq(rref.cp_drop(sym(0), rcfg), eng), 1)  # JIT
-                t_fft, Y0 = best(lambda: rref.to_freq(rref.cp_drop(sym(0), rcfg), eng))
-                t_ls, est = best(lambda: rref.ls_estimate(Y0, pilot, eng))
-                Y1 = rref.to_freq(rref.cp_drop(sym(1), rcfg), eng)
-
-                def mrc_demap():
-                    c = rref.mrc_combine(Y1, est, eng)
-                    c.bits = wref.qam_demap(c.equalized, qam)
-                    return c
-
-                t_mrc, _ = best(mrc_demap)
-                cpu = {"fft": t_fft, "ls": t_ls, "mrc": t_mrc}
-                for phase, stage, us in (("estimation", "fft", t_fft), ("estimation", "ls", t_ls),
-                                         ("demodulation", "fft", t_fft), ("demodulation", "mrc", t_mrc)):
-                    rows.append((m, cp, n, "sequential", 1, phase, stage, us, 0.0, 1))
-            summary.append({"fft_len": m, "n_antennas": n, "frames": F,
-                            "b200_us_per_symbol": {"fft": st["fft_us_per_symbol"], "ls": st["ls_us_per_pilot_symbol"],
-                                                   "mrc+demap": st["mrc_us_per_data_symbol"] + st["demap_us_per_data_symbol"],
-                                                   "fused": st["fused_us_per_symbol"]},
-                            "cpu_us_per_symbol": cpu})
-            del x
-            torch.cuda.empty_cache()
-            print(json.dumps(summary[-1]), file=sys.stderr, flush=True)
-    with open(args.sweep_csv, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(CSV_HEADER.split(","))
-        for r in rows:
-            w.writerow(r[:7] + (repr(float(r[7])), repr(float(r[8])), r[9]))
+    records, summary = sweep_cells([(n, m) for m in ffts for n in ants])
+    benchcsv.write_bench_csv(records, args.sweep_csv)
+    with open(os.path.splitext(args.sweep_csv)[0] + ".json", "w") as fh:
+        json.dump(summary, fh, indent=1)
     return {"metric": "C5 sweep: per-stage µs/symbol, b200 vs reference CPU", "csv": args.sweep_csv,
-            "configs": len(summary), "reference_cpu": bool(ref),
-            "cpu_cores_used": 1, "engine_cpu": "reference SequentialEngine (numba backend)"}
+            "configs": len(summary), "reference_cpu": reference_importable(),
+            "cpu_cores_used": 1, "engine_cpu": "reference SequentialEngine (numba backend)",
+            "min_roofline_frac": min(c["roofline_frac"] for c in summary),
+            "all_bits_equal_reference": all(c.get("bits_equal_reference", True) for c in summary)}
 
 
 def main():
@@ -759,12 +995,21 @@ def main():
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sustained-steps", type=int, default=100,
+                    help="second timed region of back-to-back steps (power-cap regime); 0 = off")
+    ap.add_argument("--oracle-frames", type=int, default=16,
+                    help="distinct frames of the benched launch checked against the CPU oracle; 0 = off")
+    ap.add_argument("--no-latency", dest="latency", action="store_false",
+                    help="skip the single-frame latency section (C1 and C3)")
+    ap.add_argument("--latency-reps", type=int, default=200)
     ap.add_argument("--exchange", default="gather", choices=["gather", "allreduce", "peer"],
                     help="C4 antenna-sharded exchange: NCCL all-gather / all-reduce, or fused peer-memory stores")
     ap.add_argument("--sweep", action="store_true", help="C5: antennas x FFT per-stage sweep -> CSV")
     ap.add_argument("--sweep-antennas", default="1,2,4,8,16,32,64,128")
     ap.add_argument("--sweep-ffts", default="64,128,256,512,1024,2048,4096")
     ap.add_argument("--sweep-csv", default="gpurun_out/sweep.csv")
+    ap.add_argument("--sweep-cells", default="8x64,16x256,64x1024,128x4096",
+                    help="compact C5 sweep (NxM cells) in the default line; '' = off")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -29,6 +29,8 @@
 // through distributed shared memory (mapa + ld.shared::cluster), so a small
 // batch spreads each frame over several SMs with results bit-identical to
 // the one-CTA-per-frame launch a large batch uses.
+#include <cmath>
+
 #include "ofdmrx_fft.cuh"
 #include "ofdmrx_internal.h"
 
@@ -549,8 +551,16 @@ bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
   // rows) never spans more than two symbols.  Few CTAs per frame keep the
   // cluster small at large batches (a GPC fits fewer 8-CTA clusters than its
   // SM count suggests, and the epilogue waits on every CTA of the frame).
-  (void)n_ant;
-  const int c = (n_data + 1 + LMAX - 1) / LMAX;
+  // Phase B re-reads each H row D times from L2; the H rows of every frame in
+  // flight (~148 SMs x LMAX lanes / V frames) must stay L2-resident or the
+  // re-reads go to HBM (C4 at V = 12: 1.45x the algorithmic DRAM reads).  So
+  // large frames get more CTAs per frame: fewer frames in flight.  Nominal
+  // constants (not the device's SM count) keep V a function of the shape.
+  constexpr double kL2Budget = 80e6, kNominalSms = 148.0;
+  const double h_bytes = 8.0 * n_ant * M;
+  int c = (n_data + 1 + LMAX - 1) / LMAX;
+  const int c_l2 = (int)std::ceil(kNominalSms * h_bytes / kL2Budget);  // = ceil(V_min / LMAX)
+  if (c_l2 > c) c = c_l2 < BMAX_CLUSTER ? c_l2 : BMAX_CLUSTER;
   if (c > BMAX_CLUSTER || c * LMAX > BMAX_V) return false;
   const int V = c * LMAX;
   // CTA mapping depends on the batch: the fewest CTAs per frame (largest

@@ -22,7 +22,7 @@ import torch
 
 from . import _lib, device
 from .errors import ContractError, InputError
-from .waveform import OfdmConfig, PilotDefinition, make_pilot
+from .waveform import OfdmConfig, PilotDefinition, as_config, make_pilot
 
 
 @dataclass
@@ -109,8 +109,7 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     accepted for compatibility and ignored.  profile=True also records the
     per-stage SM cycles of the fused kernel (FrameBatch.stage_cycles; same
     results, an instrumented build of the kernel)."""
-    if not isinstance(cfg, OfdmConfig):
-        raise ContractError("cfg must be an OfdmConfig")
+    cfg = as_config(cfg)
     dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
     x = device.as_c64(rx, dev)
     if x.dim() == 2:
@@ -340,8 +339,7 @@ def receive_captures(rx, cfg, n_data, pn=None, pilot=None, *, threshold=None, ep
     from . import sync
     from .synth import generate_pn_chips
 
-    if not isinstance(cfg, OfdmConfig):
-        raise ContractError("cfg must be an OfdmConfig")
+    cfg = as_config(cfg)
     dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
     x = device.as_c64(rx, dev)
     if x.dim() == 2:

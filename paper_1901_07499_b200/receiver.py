@@ -385,8 +385,17 @@ def run_ring_pipeline(slots, cfg, engine, pilot=None, ring_capacity=64):
     if getattr(engine, "fused", False):
         return _run_fused(slots, cfg, engine, pilot)
     estimate, symbols, timings = None, [], []
-    for slot in slots:
-        result, t = process_symbol(slot, estimate, cfg, engine, pilot=pilot)
+    it = iter(slots)
+    while True:
+        # read stage: the slot handoff (the reference times its ring read, receiver.py:328-330)
+        t0 = time.perf_counter()
+        slot = next(it, None)
+        if slot is not None:
+            np.asarray(slot.payload)
+        read_s = time.perf_counter() - t0
+        if slot is None:
+            break
+        result, t = process_symbol(slot, estimate, cfg, engine, pilot=pilot, read_seconds=read_s)
         timings.append(t)
         if isinstance(result, ChannelEstimate):
             estimate = result

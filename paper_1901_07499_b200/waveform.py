@@ -55,6 +55,21 @@ class OfdmConfig:
         return int(math.log2(self.qam_order))
 
 
+def as_config(cfg):
+    """Accept this package's OfdmConfig or any object with the reference
+    OfdmConfig's fields (e.g. ofdmrx.waveform.OfdmConfig, waveform.py:23-54),
+    so reference-built configs drive the device path unchanged."""
+    if isinstance(cfg, OfdmConfig):
+        return cfg
+    try:
+        return OfdmConfig(int(cfg.fft_len), int(cfg.cp_len), int(cfg.n_antennas), qam_order=int(cfg.qam_order),
+                          pn_len=int(getattr(cfg, "pn_len", 255)),
+                          sample_rate_hz=float(getattr(cfg, "sample_rate_hz", 10e6)))
+    except AttributeError as e:
+        from .errors import ContractError
+        raise ContractError(f"cfg must be an OfdmConfig (missing field: {e})") from None
+
+
 def default_cp(fft_len):
     """waveform.py:57-59."""
     return CANONICAL_CP.get(fft_len, max(1, fft_len // 8))
