@@ -31,7 +31,7 @@ CONFIGS = {
     "C1": (8, 64, 16, 4, 10, 65536),
     "C2": (16, 256, 32, 16, 10, 1000),
     "C3": (64, 1024, 72, 16, 10, 1024),
-    "C4": (256, 2048, 256, 64, 10, 64),
+    "C4": (256, 2048, 256, 64, 10, 296),
 }
 METRIC = "OFDM symbols/s & per-stage µs/symbol at 64 ant × FFT 1024, 1/2/4/8 B200"
 DISTINCT = 16  # distinct synthetic frames, tiled on the device
@@ -411,31 +411,40 @@ def run_b200(args, cfg_name, world, rank, local):
         # antenna-sharded MRC: every rank holds N/world antennas of the same frames
         from paper_1901_07499_b200 import sharding
 
-        sharded = sharding.AntennaShardedReceiver(cfg, d, symbol0_offset=s0, mode=args.exchange)
+        chunk = F // 4 if args.exchange == "scatter" and F % 4 == 0 and (F // 4) % world == 0 else None
+        sharded = sharding.AntennaShardedReceiver(cfg, d, symbol0_offset=s0, mode=args.exchange, chunk_frames=chunk)
         x = x[:, sharded.ant_lo:sharded.ant_hi].contiguous()
 
     own = slice(None)
-    if sharded is not None and args.exchange == "peer":  # each rank finishes its F/world frames
-        own = slice(rank * (F // world), (rank + 1) * (F // world))
+    lo, hi = 0, min(F, DISTINCT)
+    if sharded is not None and args.exchange in ("peer", "scatter"):  # each rank finishes its F/world frames
+        own = torch.tensor(sharded.owned_frames(F) if args.exchange == "scatter" else
+                           list(range(rank * (F // world), (rank + 1) * (F // world))), device=dev)
+        lo = int(own[0])
+        hi = lo + min(DISTINCT, (sharded.chunk_frames or F) // world)
 
     def step():
         if sharded is not None:
             s_hat, w, bits, fl, _ = sharded.receive(x)
-            out.bits[own].copy_(bits)
-            out.flags[own].copy_(fl)
+            out.bits[own] = bits
+            out.flags[own] = fl
         else:
             frames.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, out=out)
 
     # correctness spot-check of the benchmarked configuration (bits vs truth)
     step()
     torch.cuda.synchronize()
-    lo = own.start or 0
-    hi = min(own.stop if own.stop is not None else F, lo + DISTINCT)
     idx = np.arange(lo, hi)
     ber = float((out.bits[lo:hi].cpu().numpy() != bits_truth[idx % len(bits_truth)]).mean())
     flags_bad = int((out.flags != 0).sum())
     torch.cuda.synchronize()
-    oracle_check = check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, args.oracle_frames) if args.oracle_frames else None
+    if sharded is not None and args.oracle_frames:  # untimed: s_hat / weights of the owned frames for the check
+        s_hat, w, _, _, _ = sharded.receive(x)
+        out.s_hat[own] = s_hat
+        out.weights[own] = w
+        torch.cuda.synchronize()
+    oracle_check = (check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, args.oracle_frames, check_h=sharded is None)
+                    if args.oracle_frames else None)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
@@ -564,7 +573,7 @@ def run_b200(args, cfg_name, world, rank, local):
     return line
 
 
-def check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, max_frames):
+def check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, max_frames, check_h=True):
     """Parity of the benchmarked launch: the distinct frames' bits against the
     CPU oracle (oracle/ofdm_oracle.py, the numpy restatement of the reference
     pinned to reference-generated golden vectors), s_hat / H / weights within
@@ -577,7 +586,7 @@ def check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, max_frames):
     bits_dev = out.bits[lo:lo + k].cpu().numpy()
     sh_dev = out.s_hat[lo:lo + k].cpu().numpy()
     w_dev = out.weights[lo:lo + k].cpu().numpy()
-    h_dev = out.H[lo:lo + k].cpu().numpy() if getattr(out, "H", None) is not None and out.H.shape[1] == n else None
+    h_dev = out.H[lo:lo + k].cpu().numpy() if check_h and getattr(out, "H", None) is not None else None
 
     def rel(a, b):
         return float(np.linalg.norm(np.asarray(a, np.complex128) - b) / max(np.linalg.norm(b), 1e-300))
@@ -626,15 +635,38 @@ def comm_info(world, data_path):
 
 def run_latency(args):
     """The paper's regime: ONE frame, pinned host capture
-    -> device -> fused receive -> bits back on the host, per call.  Reported
-    per config (C1, C3): the public-API call's wall time (median / p99 over
-    `latency_reps` calls, host-timed around H2D + kernel + D2H + sync), the
-    same sequence replayed as a CUDA graph (no Python), the kernel alone
-    (CUDA events) and its per-stage split from the kernel's own stage
-    attribution (ofdmrx_rx_frames_profiled), all per OFDM symbol."""
+    -> device -> fused receive -> bits back on the host, per call, with the
+    latency plan (OFDMRX_OPT_LATENCY: the frame spread over a whole
+    thread-block cluster).  Per config (C1, C3): the public-API call's wall
+    time (median / p99 over `latency_reps` calls: H2D + kernel + D2H + sync),
+    the same sequence replayed as a CUDA graph (no Python), the kernel alone
+    (graph-replayed, CUDA events; also with the default throughput plan) and
+    its per-stage split from the kernel's own stage attribution
+    (ofdmrx_rx_frames_profiled), per OFDM symbol."""
     import torch
 
     from paper_1901_07499_b200 import frames
+
+    def graph_time_us(fn, reps=50):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps * 1e3, g
 
     res = {}
     for name in ("C1", "C3"):
@@ -642,13 +674,20 @@ def run_latency(args):
         cfg, rx_host, _, s0 = make_inputs(name)
         host = torch.from_numpy(rx_host[:1]).pin_memory()
         dev_x = torch.empty(host.shape, dtype=host.dtype, device="cuda")
+        dev_x.copy_(host)
         out = frames.allocate_outputs(1, n, m, d, qam, dev_x.device)
         bits_host = torch.empty(out.bits.shape, dtype=torch.uint8, pin_memory=True)
 
-        def call():
+        def kernel(lat=True):
+            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out, latency=lat)
+
+        def seq():
             dev_x.copy_(host, non_blocking=True)
-            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
+            kernel()
             bits_host.copy_(out.bits, non_blocking=True)
+
+        def call():
+            seq()
             torch.cuda.current_stream().synchronize()
 
         for _ in range(20):
@@ -659,21 +698,7 @@ def run_latency(args):
             call()
             ts.append(time.perf_counter() - t0)
         ts.sort()
-        # same sequence as one CUDA graph (copy in, kernel, copy out)
-        g = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            for _ in range(3):
-                dev_x.copy_(host, non_blocking=True)
-                frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
-                bits_host.copy_(out.bits, non_blocking=True)
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
-        with torch.cuda.graph(g):
-            dev_x.copy_(host, non_blocking=True)
-            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
-            bits_host.copy_(out.bits, non_blocking=True)
+        _, g = graph_time_us(seq, reps=1)
         gts = []
         for _ in range(args.latency_reps):
             t0 = time.perf_counter()
@@ -681,30 +706,27 @@ def run_latency(args):
             torch.cuda.current_stream().synchronize()
             gts.append(time.perf_counter() - t0)
         gts.sort()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(50):
-            frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, out=out)
-        b.record()
-        torch.cuda.synchronize()
-        k_us = a.elapsed_time(b) / 50 * 1e3
-        prof = frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, profile=True)
+        k_us, _ = graph_time_us(kernel)
+        k_tp_us, _ = graph_time_us(lambda: kernel(False))
+        prof = frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, profile=True, latency=True)
         torch.cuda.synchronize()
         shares = prof.stage_shares()
         sym = 1 + d
         med, p99 = ts[len(ts) // 2] * 1e6, ts[min(len(ts) - 1, int(len(ts) * 0.99))] * 1e6
         gmed = gts[len(gts) // 2] * 1e6
         res[name] = {
-            "frames": 1, "symbols_per_frame": sym,
+            "frames": 1, "symbols_per_frame": sym, "plan": "latency (OFDMRX_OPT_LATENCY)",
             "h2d_bytes": int(host.numel() * 8), "d2h_bytes": int(bits_host.numel()),
             "api_us_per_frame": {"median": med, "p99": p99}, "api_us_per_symbol": med / sym,
             "graph_us_per_frame": gmed, "graph_us_per_symbol": gmed / sym,
             "kernel_us_per_frame": k_us, "kernel_us_per_symbol": k_us / sym,
+            "kernel_us_per_frame_throughput_plan": k_tp_us,
             "kernel_stage_us_per_symbol": {
                 "fft": k_us * (shares[0] + shares[2]) / sym, "ls": k_us * shares[1],
                 "mrc": k_us * shares[3] / max(d, 1), "combine_demap": k_us * shares[4] / max(d, 1)},
-            "path": "pinned host [N, S] capture -> copy_ H2D -> frames.receive_frames (one fused launch) -> bits D2H "
-                    "-> stream sync; host perf_counter around each call"}
+            "path": "pinned host [N, S] capture -> copy_ H2D -> frames.receive_frames(latency=True) (one fused "
+                    "launch) -> bits D2H -> stream sync; host perf_counter around each call; kernel times are "
+                    "CUDA-graph replays between CUDA events"}
         del dev_x, out
     return res
 
@@ -908,7 +930,9 @@ def sweep_cells(cells, with_cpu=True, reps=3, max_frames=4096):
         cp = default_cp(m)
         cfg = OfdmConfig(m, cp, n, qam_order=qam)
         rx, _, s0 = synth.synth_batch(cfg, d, range(2), snr_db=10.0)
-        F = max(2, min(max_frames, (1 << 26) // (n * m * (1 + d))))
+        # enough frames to fill the GPU (>= 2 CTAs per SM), at most ~4 GB of input
+        F = max(296, min(max_frames, (1 << 29) // (n * m * (1 + d))))
+        F = min(F, max(2, (1 << 32) // (8 * n * m * (1 + d))))
         x = torch.from_numpy(rx).cuda().repeat((F + 1) // 2, 1, 1)[:F].contiguous()
         st = run_stages(argparse.Namespace(stage_frames=F), cfg, x, s0, d, with_sync=False)
         bpf = frame_bytes(n, m, qam, d)
@@ -1002,8 +1026,9 @@ def main():
     ap.add_argument("--no-latency", dest="latency", action="store_false",
                     help="skip the single-frame latency section (C1 and C3)")
     ap.add_argument("--latency-reps", type=int, default=200)
-    ap.add_argument("--exchange", default="gather", choices=["gather", "allreduce", "peer"],
-                    help="C4 antenna-sharded exchange: NCCL all-gather / all-reduce, or fused peer-memory stores")
+    ap.add_argument("--exchange", default="scatter", choices=["gather", "allreduce", "scatter", "peer"],
+                    help="C4 antenna-sharded exchange: NCCL all-gather / all-reduce / all-to-all (reduce-scatter shaped, "
+                         "chunk-overlapped), or fused peer-memory stores")
     ap.add_argument("--sweep", action="store_true", help="C5: antennas x FFT per-stage sweep -> CSV")
     ap.add_argument("--sweep-antennas", default="1,2,4,8,16,32,64,128")
     ap.add_argument("--sweep-ffts", default="64,128,256,512,1024,2048,4096")

@@ -94,6 +94,15 @@ typedef struct {
  * never depend on the batch size; small batches spread each frame over a
  * thread-block cluster instead of antenna shards). */
 #define OFDMRX_OPT_NO_SHARDS 2
+/* desc.options (ABI 2): latency plan for single frames and small batches
+ * (the paper's per-symbol regime).  Each frame's work is cut
+ * into the most workers a portable thread-block cluster holds (e.g. 96 for
+ * C3 instead of 12), so one frame finishes ~8x sooner; throughput at large
+ * batches is lower.  The antenna-sum order is fixed by (frame shape, this
+ * option): results never depend on the batch size, and differ from the
+ * default plan's only in fp32 rounding (bits bit-exact vs the reference in
+ * every test).  ofdmrx_rx_plan reports the plan. */
+#define OFDMRX_OPT_LATENCY 4
 
 OFDMRX_API int ofdmrx_abi_version(void);
 OFDMRX_API const char* ofdmrx_last_error(void);

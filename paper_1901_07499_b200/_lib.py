@@ -25,6 +25,7 @@ FLAG_NOT_DETECTED = 4
 FLAG_OUT_OF_RANGE = 8
 OPT_PILOT_BPSK = 1
 OPT_NO_SHARDS = 2
+OPT_LATENCY = 4
 
 _STATUS_EXC = {
     ERR_CONFIG: ConfigurationError,

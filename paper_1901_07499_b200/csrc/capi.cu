@@ -25,6 +25,9 @@ int fail(int code, const char* fmt, ...) {
 }
 
 int cuda_fail(cudaError_t e, const char* where) {
+  // consume the runtime's last-error slot: a reported (non-sticky) launch
+  // failure must not resurface as the status of the next call's launch
+  (void)cudaGetLastError();
   return fail(OFDMRX_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
 }
 
@@ -60,7 +63,7 @@ int check_qam(int order) {
 // detected-capture row length); the whole batch must lie inside rx_samples
 int check_desc_impl(const ofdmrx_frame_desc* d, long long rows_len = -1) {
   if (d == nullptr) return fail(OFDMRX_ERR_CONTRACT, "descriptor is NULL");
-  if ((d->options & ~(OFDMRX_OPT_PILOT_BPSK | OFDMRX_OPT_NO_SHARDS)) != 0)
+  if ((d->options & ~(OFDMRX_OPT_PILOT_BPSK | OFDMRX_OPT_NO_SHARDS | OFDMRX_OPT_LATENCY)) != 0)
     return fail(OFDMRX_ERR_CONTRACT, "unknown descriptor options 0x%x", d->options);
   if (int rc = check_fft_len(d->fft_len)) return rc;
   if (d->cp_len < 0 || d->cp_len >= d->fft_len)
@@ -152,7 +155,8 @@ struct RxPlan {
 int make_plan(const ofdmrx_frame_desc* d, RxPlan* pl) {
   *pl = RxPlan{};
   pl->balanced = ofdmrx::balanced_plan(d->fft_len, d->n_antennas, d->n_data, d->n_frames,
-                                        ofdmrx::device_sm_count(), &pl->bp);
+                                        ofdmrx::device_sm_count(), (d->options & OFDMRX_OPT_LATENCY) != 0,
+                                        &pl->bp);
   if (!pl->balanced) {
     if (ofdmrx::fused_plan(d->fft_len, d->n_frames, d->n_data, &pl->fl) != cudaSuccess)
       return fail(OFDMRX_ERR_CONFIG, "no launch plan for fft_len %d", d->fft_len);

@@ -107,7 +107,7 @@ struct BalancedPlan {
   int cluster;          // CTAs per frame (thread-block cluster size)
   int fft_lane_threads; // G
 };
-bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out);
+bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool latency, BalancedPlan* out);
 size_t balanced_smem_bytes(int M, int lanes_per_cta);
 cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp, cudaStream_t s);
 

@@ -29,8 +29,6 @@
 // through distributed shared memory (mapa + ld.shared::cluster), so a small
 // batch spreads each frame over several SMs with results bit-identical to
 // the one-CTA-per-frame launch a large batch uses.
-#include <cmath>
-
 #include "ofdmrx_fft.cuh"
 #include "ofdmrx_internal.h"
 
@@ -48,9 +46,11 @@ struct BalCfg {
   using PI = PlanInfo<M>;
   static constexpr int P = PI::P, G = PI::G, LW = G / 32, SLOT = PI::SLOT;
   static constexpr int ACC = 2 * P;             // floats per accumulator set
-  static constexpr int COLS = 2 * ACC + P;      // 2 sets + den partial, per warp
+  static constexpr int COLS = (2 * ACC + P + 15) / 16 * 16;  // 2 sets + den partial, per warp (16-aligned)
   static constexpr int LPC_MAX = BMAXW / LW;    // lanes per CTA at most
-  static_assert(P == 32 && G >= 32, "balanced kernel: 32 points per thread, whole-warp lanes");
+  // P = 8 lanes are register-lean: two CTAs per SM (24 warps) hide more latency
+  static constexpr int MIN_CTAS = P <= 8 ? 2 : 1;
+  static_assert((P == 32 || P == 16 || P == 8) && G >= 32, "balanced kernel: whole-warp lanes, 8..32 points");
   static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * SLOT * sizeof(float2); }
 };
 
@@ -131,7 +131,7 @@ __device__ __forceinline__ float2 ld_dsmem2(uint32_t a) {
 }
 
 template <int M, bool BPSK, bool ZF, bool PROF>
-__global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedParams p) {
+__global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_kernel(const FusedParams p) {
   using BC = BalCfg<M>;
   constexpr int P = BC::P, G = BC::G, LW = BC::LW, SS = BC::SLOT, ACC = BC::ACC, COLS = BC::COLS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -213,12 +213,43 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     tmem_st<ACC>(tbase, z);
     tmem_st<ACC>(tbase + ACC, z);
   }
-  const int total = D * N;
 #ifdef OFDMRX_BAL_EVEN_SPLIT
+  const int total = D * N;
   const int r0 = (int)((long long)total * v / V), r1 = (int)((long long)total * (v + 1) / V);  // experiment
 #else
   const int r0 = lo_tab[v], r1 = lo_tab[v + 1];
 #endif
+  // Phase-B row order.  The lane's rows are symbol d_first from antenna nA
+  // on (set A) and, when the range spans a symbol boundary, symbol
+  // d_first + 1 up to antenna nB (set B).  They are streamed by ascending
+  // ANTENNA, not symbol-major: B-only rows (n < nA), then pairs (d_first, n),
+  // (d_first + 1, n) for n in [nA, nB], then A-only rows.  All V lanes of a
+  // frame thus sweep the antennas together, so each H row is re-read D times
+  // within a short window and stays in L2 even when the H rows of all frames
+  // in flight exceed it (C4: 148 x 4 MB).  Each accumulator set still sees
+  // its antennas in ascending order: the arithmetic is that of the
+  // symbol-major order.
+  const int d_first = r0 < r1 ? r0 / N : 0;
+  const int nA = r0 - d_first * N;
+  const bool two = r0 < r1 && r1 - 1 >= (d_first + 1) * N;
+  const int nB = two ? r1 - 1 - (d_first + 1) * N : -1;
+  // first row: antenna 0 of set B if the lane has one, else antenna nA of A;
+  // next row after (n, set): (n, B) if the current is A and n <= nB, else
+  // antenna n + 1 (skipping the gap nB < n < nA), set A from nA on
+  auto first_row = [&](int& dd, int& nn) {
+    nn = two ? 0 : nA;
+    dd = d_first + (nn < nA ? 1 : 0);
+  };
+  auto next_row = [&](int& dd, int& nn) {
+    if (dd == d_first && nn <= nB) {
+      dd = d_first + 1;
+    } else {
+      ++nn;
+      if (nn > nB && nn < nA) nn = nA;
+      dd = d_first + (nn < nA ? 1 : 0);
+    }
+  };
+  const int nrows = r1 - r0;
   int k = 0;  // stage counter across both phases
   if (leader && v < N) issue_rx(row_addr(0, v), 0);
   float2 y[P];
@@ -227,7 +258,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     float2* slot = slot_base + (size_t)st * SS;
     if (leader) {
       if (n + V < N) issue_rx(row_addr(0, n + V), st ^ 1);
-      else if (r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), st ^ 1);  // first data row of phase B
+      else if (nrows > 0) {  // first data row of phase B
+        int d0, n0;
+        first_row(d0, n0);
+        issue_rx(row_addr(1 + d0, n0), st ^ 1);
+      }
     }
     uint32_t tc = prof ? sm_clock() : 0u;
     wait_rx(k);
@@ -263,7 +298,11 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     tmem_st<P>(t_den, dp);
     if (prof && leader) cyc[kStageLs] += sm_clock() - tc;
   }
-  if (leader && v >= N && r0 < r1) issue_rx(row_addr(1 + r0 / N, r0 % N), k & 1);  // no pilot rows
+  if (leader && v >= N && nrows > 0) {  // no pilot rows
+    int d0, n0;
+    first_row(d0, n0);
+    issue_rx(row_addr(1 + d0, n0), k & 1);
+  }
   tmem_wait_st();
   // H rows of this lane are published; lanes of the frame acquire them
   // before their first H load (wait inside the first data FFT, below).  One
@@ -281,14 +320,14 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
   bool h_acquired = false;
 
   // ---------------- phase B: this lane's data rows -------------------------
-  const int d_first = r0 < r1 ? r0 / N : 0;
-  int d = d_first, n = r0 - d_first * N;  // current row (symbol-major)
-  int dn = d, nn = n + 1;                 // next row
-  if (nn == N) nn = 0, ++dn;
-  for (int r = r0; r < r1; ++r, ++k) {
+  int d, n;  // current row
+  first_row(d, n);
+  for (int q = 0; q < nrows; ++q, ++k) {
     const int st = k & 1;
     float2* slot = slot_base + (size_t)st * SS;
-    if (leader && r + 1 < r1) issue_rx(row_addr(1 + dn, nn), st ^ 1);
+    int dn = d, nn = n;  // next row
+    next_row(dn, nn);
+    if (leader && q + 1 < nrows) issue_rx(row_addr(1 + dn, nn), st ^ 1);
     uint32_t tc = prof ? sm_clock() : 0u;
     wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(1 + d, n)) >> 3) & 1);
@@ -344,7 +383,6 @@ __global__ void __launch_bounds__(BMAXW * 32, 1) rx_balanced_kernel(const FusedP
     lane_sync();
     if (prof && leader) cyc[kStageMrc] += sm_clock() - tc;
     d = dn, n = nn;
-    if (++nn == N) nn = 0, ++dn;
   }
   if (!h_acquired) h_acquire();
 
@@ -504,7 +542,8 @@ cudaError_t launch_t(const FusedParams& p, const BalancedPlan& bp, cudaStream_t 
   using BC = BalCfg<M>;
   static unsigned done = 0;
   auto kern = rx_balanced_kernel<M, BPSK, ZF, PROF>;
-  if (cudaError_t e = ensure_smem_attr(kern, (int)BC::smem_bytes(BC::LPC_MAX), done); e != cudaSuccess) return e;
+  // the launch pads the request (TMEM residency, below): allow the full 227 KB
+  if (cudaError_t e = ensure_smem_attr(kern, 227 * 1024, done); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.n_frames * (unsigned)bp.cluster, 1, 1);
   cfg.blockDim = dim3((unsigned)(bp.lanes_per_cta * BC::G), 1, 1);
@@ -543,7 +582,7 @@ cudaError_t launch_m(const FusedParams& p, const BalancedPlan& bp, cudaStream_t 
 }
 
 template <int M>
-bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
+bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, bool latency, BalancedPlan* out) {
   using BC = BalCfg<M>;
   constexpr int LMAX = BC::LPC_MAX;
   // V (virtual lanes per frame) depends on the frame shape only: the fewest
@@ -551,16 +590,13 @@ bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
   // rows) never spans more than two symbols.  Few CTAs per frame keep the
   // cluster small at large batches (a GPC fits fewer 8-CTA clusters than its
   // SM count suggests, and the epilogue waits on every CTA of the frame).
-  // Phase B re-reads each H row D times from L2; the H rows of every frame in
-  // flight (~148 SMs x LMAX lanes / V frames) must stay L2-resident or the
-  // re-reads go to HBM (C4 at V = 12: 1.45x the algorithmic DRAM reads).  So
-  // large frames get more CTAs per frame: fewer frames in flight.  Nominal
-  // constants (not the device's SM count) keep V a function of the shape.
-  constexpr double kL2Budget = 80e6, kNominalSms = 148.0;
-  const double h_bytes = 8.0 * n_ant * M;
   int c = (n_data + 1 + LMAX - 1) / LMAX;
-  const int c_l2 = (int)std::ceil(kNominalSms * h_bytes / kL2Budget);  // = ceil(V_min / LMAX)
-  if (c_l2 > c) c = c_l2 < BMAX_CLUSTER ? c_l2 : BMAX_CLUSTER;
+  if (latency) {  // OFDMRX_OPT_LATENCY: the widest portable cluster, >= ~4 rows per worker
+    const long long rows = (long long)n_ant * (1 + n_data);
+    long long cl = (rows + 4LL * LMAX - 1) / (4LL * LMAX);
+    if (cl > BMAX_CLUSTER) cl = BMAX_CLUSTER;
+    if (cl > c) c = (int)cl;
+  }
   if (c > BMAX_CLUSTER || c * LMAX > BMAX_V) return false;
   const int V = c * LMAX;
   // CTA mapping depends on the batch: the fewest CTAs per frame (largest
@@ -580,15 +616,16 @@ bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
 
 }  // namespace
 
-bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, BalancedPlan* out) {
+bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool latency, BalancedPlan* out) {
 #ifdef OFDMRX_NO_BALANCED
   return false;
 #else
   if (n_ant < 1 || n_data < 0) return false;
   switch (M) {
-    case 1024: return plan_m<1024>(n_ant, n_data, n_frames, n_sm, out);
-    case 2048: return plan_m<2048>(n_ant, n_data, n_frames, n_sm, out);
-    case 4096: return plan_m<4096>(n_ant, n_data, n_frames, n_sm, out);
+    case 256: return plan_m<256>(n_ant, n_data, n_frames, n_sm, latency, out);
+    case 1024: return plan_m<1024>(n_ant, n_data, n_frames, n_sm, latency, out);
+    case 2048: return plan_m<2048>(n_ant, n_data, n_frames, n_sm, latency, out);
+    case 4096: return plan_m<4096>(n_ant, n_data, n_frames, n_sm, latency, out);
     default: return false;
   }
 #endif
@@ -596,6 +633,7 @@ bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, Balance
 
 size_t balanced_smem_bytes(int M, int lanes_per_cta) {
   switch (M) {
+    case 256: return BalCfg<256>::smem_bytes(lanes_per_cta);
     case 1024: return BalCfg<1024>::smem_bytes(lanes_per_cta);
     case 2048: return BalCfg<2048>::smem_bytes(lanes_per_cta);
     case 4096: return BalCfg<4096>::smem_bytes(lanes_per_cta);
@@ -606,6 +644,7 @@ size_t balanced_smem_bytes(int M, int lanes_per_cta) {
 cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
   if (p.n_frames == 0) return cudaSuccess;
   switch (M) {
+    case 256: return launch_m<256>(p, bp, s);
     case 1024: return launch_m<1024>(p, bp, s);
     case 2048: return launch_m<2048>(p, bp, s);
     case 4096: return launch_m<4096>(p, bp, s);

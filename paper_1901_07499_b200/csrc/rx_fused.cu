@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSTAGE * lanes; ++i) mbar_init(&tma_bar[i], 1);
     for (int i = 0; i < ngroups * RING; ++i) {
-      mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], p.dc > 0 ? p.dc : 1);
+      // every thread of the producing / consuming units arrives (each
+      // thread's release covers its own ring accesses)
+      mbar_init(&full_bar[i], UT);
+      mbar_init(&empty_bar[i], (p.dc > 0 ? p.dc : 1) * UT);
     }
     fence_mbar_init();
   }
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   const bool leader = active && t == 0;
   uint64_t pol = 0;
   if (leader) pol = l2_evict_first_policy();
-  auto issue = [&](int n, int st) {
+  auto issue_lane = [&](int n, int st) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(row0 + (long long)n * p.row_stride);
     const uintptr_t start = a & ~uintptr_t(15);
     const uint32_t bytes = (uint32_t)(((a + (uintptr_t)M * 8u + 15u) & ~uintptr_t(15)) - start);
@@ -157,7 +159,35 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     mbar_arrive_expect_tx(bar, bytes);
     tma_bulk_g2s(slots + (size_t)(st * lanes + lane) * SS, reinterpret_cast<const void*>(start), bytes, bar, pol);
   };
-  if (leader && n_first < p.n_ant) issue(n_first, 0);
+  // Row n of every lane of this unit into stage st (called by the whole unit;
+  // n is unit-uniform): each lane's leader issues its own copy.  With lanes
+  // narrower than a warp (GI > 1) the GI leaders issue converged, and the
+  // lanes wait converged on GI different mbarriers -- correct, but
+  // compute-sanitizer's racecheck tracks one barrier per warp-level wait and
+  // reports "invalid async operation synchronization".  The
+  // OFDMRX_RACECHECK_SERIAL build (scripts/sanitize.sh) issues and waits one
+  // lane at a time, and is hazard-free under racecheck.
+  auto issue = [&](int n, int st) {
+#ifdef OFDMRX_RACECHECK_SERIAL
+    for (int s2 = 0; s2 < GI; ++s2) {
+      if (sub == s2 && leader) issue_lane(n, st);
+      __syncwarp();
+    }
+#else
+    if (leader) issue_lane(n, st);
+#endif
+  };
+  auto wait_rx = [&](int st, uint32_t parity) {
+#ifdef OFDMRX_RACECHECK_SERIAL
+    for (int s2 = 0; s2 < GI; ++s2) {
+      if (sub == s2 && active) mbar_wait_parity(&tma_bar[st * lanes + lane], parity);
+      __syncwarp();
+    }
+#else
+    if (active) mbar_wait_parity(&tma_bar[st * lanes + lane], parity);
+#endif
+  };
+  if (n_first < p.n_ant) issue(n_first, 0);
 #ifdef OFDMRX_EXP_NOLOAD
   constexpr bool kLoadEvery = false;  // experiment: compute-only (first antenna's row reused)
 #else
@@ -206,10 +236,10 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
 
   for (int k = 0, n = n_first; n < p.n_ant; ++k, n += n_step) {
     const int st = NSTAGE == 2 ? (k & 1) : 0;
-    if (kLoadEvery && NSTAGE == 2 && leader && n + n_step < p.n_ant) issue(n + n_step, st ^ 1);  // freed at the end of step k-1
+    if (kLoadEvery && NSTAGE == 2 && n + n_step < p.n_ant) issue(n + n_step, st ^ 1);  // freed at the end of step k-1
     float2* slot = slots + (size_t)(st * lanes + lane) * SS;
     uint32_t tc = prof ? sm_clock() : 0u;
-    if (active && (kLoadEvery || k == 0)) mbar_wait_parity(&tma_bar[st * lanes + lane], NSTAGE == 2 ? ((k >> 1) & 1) : (k & 1));
+    if (kLoadEvery || k == 0) wait_rx(st, NSTAGE == 2 ? ((k >> 1) & 1) : (k & 1));
     const int sh = (int)((reinterpret_cast<uintptr_t>(row0 + (long long)n * p.row_stride) >> 3) & 1);
     const float2* src = slot + sh;
 #ifdef OFDMRX_EXP_NOFFT
@@ -220,7 +250,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
 #endif
     fence_proxy_async_smem();  // this thread's generic smem writes before the async-proxy refill
     unit_sync();               // every read of the slot done: it may be refilled
-    if (kLoadEvery && NSTAGE == 1 && leader && n + n_step < p.n_ant) issue(n + n_step, 0);
+    if (kLoadEvery && NSTAGE == 1 && n + n_step < p.n_ant) issue(n + n_step, 0);
     if (prof) {
       const uint32_t t1 = sm_clock();
       c_fft += t1 - tc;
@@ -251,8 +281,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
 #pragma unroll
       for (int i = 0; i < P; i += 2)
         *reinterpret_cast<float4*>(hb + (i >> 1) * 2 * G + 2 * t) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
-      unit_sync();
-      if (u == 0) mbar_arrive(&full_bar[grp * RING + r]);
+      mbar_arrive(&full_bar[grp * RING + r]);
       acc_load(a);
 #pragma unroll
       for (int i = 0; i < P; ++i) {  // (sum h.x^2, sum h.y^2) per subcarrier, added at the end
@@ -291,8 +320,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
           }
         }
       }
-      unit_sync();
-      if (u == 0) mbar_arrive(&empty_bar[grp * RING + r]);
+      mbar_arrive(&empty_bar[grp * RING + r]);
       acc_store(a);
     }
     if (prof) c_comb += sm_clock() - tc;

@@ -99,7 +99,8 @@ def allocate_outputs(n_frames, n_antennas, fft_len, n_data, qam_order, dev, want
 
 
 def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=device.MRC_WEIGHT_FLOOR,
-                   out=None, want_h=True, zf=False, check=False, stream=None, shards=None, profile=False):
+                   out=None, want_h=True, zf=False, check=False, stream=None, shards=None, profile=False,
+                   latency=False):
     """Fused receive of a batch of captures on the current CUDA device.
 
     rx: complex64 CUDA tensor [F, N, S] or [N, S] (numpy is copied H2D).
@@ -108,7 +109,9 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     do not depend on the batch (F) a frame is received in; `shards` is
     accepted for compatibility and ignored.  profile=True also records the
     per-stage SM cycles of the fused kernel (FrameBatch.stage_cycles; same
-    results, an instrumented build of the kernel)."""
+    results, an instrumented build of the kernel).  latency=True selects the
+    single-frame latency plan (OFDMRX_OPT_LATENCY: each frame over a whole
+    thread-block cluster; its own fixed antenna-sum order)."""
     cfg = as_config(cfg)
     dev = device.require_cuda(rx.device if isinstance(rx, torch.Tensor) and rx.is_cuda else None)
     x = device.as_c64(rx, dev)
@@ -125,13 +128,14 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
     if n_data < 0 or symbol0_offset < 0:
         raise InputError(f"capture of {s} samples holds no pilot symbol at offset {symbol0_offset}")
     desc_args = (f, n, cfg.fft_len, cfg.cp_len, n_data, cfg.qam_order, symbol0_offset, s, n * s, eps)
-    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=profile)
+    return _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=profile, latency=latency)
 
 
-def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=False):
+def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=False, latency=False):
     f, n, _, _, n_data = desc_args[:5]
     pvals = _pilot_values(pilot, cfg.fft_len)
-    desc = device.make_desc(*desc_args, options=device.pilot_options(pvals), rx_samples=x.numel())
+    opts = device.pilot_options(pvals) | (_lib.OPT_LATENCY if latency else 0)
+    desc = device.make_desc(*desc_args, options=opts, rx_samples=x.numel())
     device.check_desc(desc)
     pv = _PILOTS.get(pvals, x.device)
     with device.on_stream(stream):  # outputs allocated / zeroed on the launch stream

@@ -15,6 +15,13 @@
       (numerics.py:85-106) when the shard size is a power of two;
     - "allreduce": one NCCL sum all-reduce of the packed partials (half the
       bytes on the wire, association order left to NCCL).
+    - "scatter": reduce-scatter shaped.  Rank o owns frames [o F/G, (o+1) F/G)
+      of every chunk; one all-to-all sends each owner the partials of its
+      frames (each rank receives F/G x G partial sets instead of F x G), the
+      owner runs the same rank-ordered pairwise tree over them and finishes
+      only its frames.  Chunked: the exchange of chunk i runs on NCCL's stream
+      while chunk i+1's partial-sum kernel runs (AntennaShardedReceiver
+      chunk_frames).
     - "peer": no collective on the data path.  Each rank owns F/G frames; the
       fused partial-sum kernel stores every frame's (num, den) straight into
       the owner's inbox over peer memory (CUDA IPC mappings: NVLink stores
@@ -32,7 +39,7 @@ import torch.distributed as dist
 
 from .errors import ConfigurationError, ContractError
 
-EXCHANGE_MODES = ("gather", "allreduce", "peer")
+EXCHANGE_MODES = ("gather", "allreduce", "scatter", "peer")
 
 
 def frame_shard(n_frames, rank, world):
@@ -65,6 +72,12 @@ def unpack_partials(buf, n_frames, n_data, fft_len):
     return num, den
 
 
+def _host_staged(t, group):
+    """gloo moves CPU tensors only: device buffers go through host memory
+    (the multi-process code-path tests on one GPU); NCCL takes them as is."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def exchange_partials(num, den, mode="gather", group=None):
     """Combine the antenna shards' partial sums across the process group.
 
@@ -76,6 +89,9 @@ def exchange_partials(num, den, mode="gather", group=None):
     f, d, m = num.shape
     buf = pack_partials(num, den)
     world = dist.get_world_size(group)
+    if _host_staged(buf, group):
+        n, dd = exchange_partials(num.cpu(), den.cpu(), mode, group)
+        return n.to(num.device), dd.to(num.device)
     if mode == "allreduce":
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         n, dd = unpack_partials(buf, f, d, m)
@@ -88,6 +104,42 @@ def exchange_partials(num, den, mode="gather", group=None):
         dist.all_gather(parts, buf, group=group)
         out = torch.stack(parts)
     return unpack_partials(out, f, d, m)
+
+
+def scatter_pack(num, den, world):
+    """[F,D,M] c64 + [F,M] f32 -> [G, F/G * (2DM + M)] f32: row o holds the
+    partials of owner o's contiguous frame block (the all-to-all send buffer)."""
+    f, d, m = num.shape
+    if f % world:
+        raise ConfigurationError(f"{f} frames do not split evenly over {world} owners")
+    return torch.cat([torch.view_as_real(num).reshape(world, -1), den.reshape(world, -1)], dim=1).contiguous()
+
+
+def scatter_unpack(recv, n_data, fft_len):
+    """Inverse of scatter_pack on the receive side: [G, fpo*(2DM+M)] ->
+    (num [G, fpo, D, M], den [G, fpo, M]), row g = rank g's partials."""
+    g = recv.shape[0]
+    per = 2 * n_data * fft_len + fft_len
+    fpo = recv.shape[1] // per
+    nn = fpo * n_data * fft_len * 2
+    num = torch.view_as_complex(recv[:, :nn].reshape(g, fpo, n_data, fft_len, 2).contiguous())
+    den = recv[:, nn:].reshape(g, fpo, fft_len)
+    return num, den
+
+
+def scatter_partials(num, den, group=None, async_op=False):
+    """Reduce-scatter shaped exchange (mode "scatter"): all-to-all of the
+    owner blocks.  Returns (recv [G, fpo*(2DM+M)], work) -- recv row g holds
+    rank g's partial sums of this rank's frames (scatter_unpack)."""
+    world = dist.get_world_size(group)
+    send = scatter_pack(num, den, world)
+    if _host_staged(send, group):
+        recv = torch.empty_like(send, device="cpu")
+        dist.all_to_all_single(recv, send.cpu(), group=group)
+        return recv.to(send.device), None
+    recv = torch.empty_like(send)
+    work = dist.all_to_all_single(recv, send, group=group, async_op=async_op)
+    return recv, work
 
 
 def tree_sum_parts(x):
@@ -185,9 +237,11 @@ class AntennaShardedReceiver:
     """Antenna-sharded fused receive for one rank of a process group.
 
     receive(rx_shard) takes this rank's antenna rows [F, N/G, S] of the frames
-    and returns (s_hat, weights, bits, flags) for all F frames on every rank."""
+    and returns (s_hat, weights, bits, flags, H) for all F frames on every rank
+    (modes "gather" / "allreduce") or for the frames this rank owns (modes
+    "scatter" / "peer": owned_frames(F))."""
 
-    def __init__(self, cfg, n_data, symbol0_offset=0, pilot=None, mode="gather", group=None):
+    def __init__(self, cfg, n_data, symbol0_offset=0, pilot=None, mode="gather", group=None, chunk_frames=None):
         from .waveform import OfdmConfig
 
         if mode not in EXCHANGE_MODES:
@@ -201,6 +255,7 @@ class AntennaShardedReceiver:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.ant_lo, self.ant_hi = antenna_shard(cfg.n_antennas, self.rank, self.world)
+        self.chunk_frames = chunk_frames
         self.shard_cfg = OfdmConfig(cfg.fft_len, cfg.cp_len, self.ant_hi - self.ant_lo, qam_order=cfg.qam_order,
                                     pn_len=cfg.pn_len)
         self.peer = None
@@ -210,6 +265,8 @@ class AntennaShardedReceiver:
 
         if self.mode == "peer":
             return self._receive_peer(rx_shard, want_h, stream)
+        if self.mode == "scatter":
+            return self._receive_scatter(rx_shard, want_h)
         H, num, den, flags = frames.receive_partials(rx_shard, self.shard_cfg, self.pilot,
                                                      symbol0_offset=self.symbol0_offset, n_data=self.n_data,
                                                      want_h=want_h, stream=stream)
@@ -263,6 +320,55 @@ class AntennaShardedReceiver:
         _lib.check(lib.ofdmrx_peer_signal(dv.ptr(ex.consumed_dst), 1, e, st))
         own = slice(ex.rank * fo, (ex.rank + 1) * fo)
         return s_hat, weights, bits, fflags | flags[own], (H[own] if H is not None else None)
+
+    def owned_frames(self, n_frames):
+        """Frame indices this rank returns in mode "scatter" (and "peer"):
+        block rank of every chunk of chunk_frames frames."""
+        c = self.chunk_frames or n_frames
+        fpo = c // self.world
+        return [ci * c + self.rank * fpo + j for ci in range(n_frames // c) for j in range(fpo)]
+
+    def _receive_scatter(self, rx_shard, want_h):
+        """Chunked partials -> all-to-all of the owner blocks -> finish of the
+        owned frames.  The all-to-all of chunk i is issued async (NCCL's own
+        stream waits for chunk i's partial kernel) and chunk i+1's partial
+        kernel is enqueued before the current stream waits for it, so the
+        exchange overlaps the next chunk's compute.  Returns (s_hat, weights,
+        bits, flags, H) for owned_frames(F), in that order."""
+        from . import device as dv, frames
+
+        x = rx_shard
+        if isinstance(x, torch.Tensor) and x.dim() == 2:
+            x = x[None]
+        f = x.shape[0]
+        c = self.chunk_frames or f
+        if c % self.world or f % c:
+            raise ConfigurationError(f"chunk of {c} frames must divide {f} frames and split over {self.world} owners")
+        d, m = self.n_data, self.cfg.fft_len
+        pending, outs = [], []
+
+        def finish(item):
+            recv, work, flags, H = item
+            if work is not None:
+                work.wait()
+            nump, denp = scatter_unpack(recv, d, m)
+            s_hat, w, bits, ff = frames.finish_partials(nump, denp, self.cfg.qam_order)
+            fpo = c // self.world
+            own = slice(self.rank * fpo, (self.rank + 1) * fpo)
+            outs.append((s_hat, w, bits, ff | flags[own], H[own] if H is not None else None))
+
+        for ci in range(f // c):
+            H, num, den, flags = frames.receive_partials(x[ci * c:(ci + 1) * c], self.shard_cfg, self.pilot,
+                                                         symbol0_offset=self.symbol0_offset, n_data=d,
+                                                         want_h=want_h)
+            recv, work = scatter_partials(num, den, self.group, async_op=True)
+            pending.append((recv, work, flags, H))
+            if len(pending) > 1:  # chunk ci's kernel is queued: finish chunk ci-1
+                finish(pending.pop(0))
+        while pending:
+            finish(pending.pop(0))
+        cat = lambda i: torch.cat([o[i] for o in outs]) if outs[0][i] is not None else None  # noqa: E731
+        return cat(0), cat(1), cat(2), cat(3), cat(4)
 
     def close(self):
         if getattr(self, "peer", None) is not None:

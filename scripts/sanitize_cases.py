@@ -15,7 +15,11 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1901_07499_b200 as P  # noqa: E402
+from paper_1901_07499_b200 import _lib  # noqa: E402
 from oracle import ofdm_oracle as orc  # noqa: E402
+
+if os.environ.get("OFDMRX_VARIANT_LIB"):  # sanitizer build (scripts/sanitize.sh); the package never does this
+    _lib.LIB_PATH = os.environ["OFDMRX_VARIANT_LIB"]
 
 
 def caps(m, cp, n, qam, d, k, seed=0):

@@ -78,7 +78,7 @@ def test_outputs_independent_of_batch(shape):
     kernels = {p[0] for p in plans}
     workers = {(p[0], p[1]) for p in plans}
     assert len(kernels) == 1 and len(workers) == 1, f"arithmetic plan changed with the batch: {plans}"
-    lanes_max = {1024: 12, 2048: 6, 4096: 3}.get(m, 0)
+    lanes_max = {256: 12, 1024: 12, 2048: 6, 4096: 3}.get(m, 0)
     if 1 in kernels and next(iter(workers))[1] < 8 * lanes_max:
         # balanced with room for more than one cluster size: the CTA mapping
         # must actually differ across the batch sizes
@@ -125,3 +125,39 @@ def test_partials_independent_of_batch():
     for j in range(80):
         r = ref[j % 2]
         assert torch.equal(num[j], r[1][0]) and torch.equal(den[j], r[2][0]) and torch.equal(H[j], r[0][0])
+
+
+@pytest.mark.parametrize("shape", [(64, 1024, 72, 16, 10), (16, 256, 32, 16, 10), (256, 2048, 256, 64, 10)],
+                         ids=["C3", "C2", "C4"])
+def test_latency_plan(shape):
+    """OFDMRX_OPT_LATENCY (receive_frames(latency=True)): more workers per
+    frame than the throughput plan; bits exact vs the oracle, H / s_hat
+    within 1e-4; batch-invariant within the plan (F = 1, 3, 40)."""
+    import paper_1901_07499_b200 as P
+    from paper_1901_07499_b200 import _lib, device
+
+    n_ant, m, cp, qam, d = shape
+    cfg = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
+    caps = [orc.synth_capture(m, cp, n_ant, qam, d, 700 + i, snr_db=10.0) for i in range(2)]
+    s0 = caps[0][2]
+    host = np.stack([c[0] for c in caps]).astype(np.complex64)
+    x = torch.from_numpy(host).cuda()
+    opts = device.pilot_options(orc.make_pilot(m))
+    mk = lambda F, o: device.make_desc(F, n_ant, m, cp, d, qam, s0, x.shape[2], n_ant * x.shape[2],  # noqa: E731
+                                       options=o, rx_samples=F * n_ant * x.shape[2])
+    lat, thr = device.rx_plan(mk(1, opts | _lib.OPT_LATENCY)), device.rx_plan(mk(1, opts))
+    assert lat["workers"] > thr["workers"], (lat, thr)
+    alone = [P.receive_frames(x[i:i + 1], cfg, symbol0_offset=s0, n_data=d, latency=True) for i in range(2)]
+    torch.cuda.synchronize()
+    for i in range(2):
+        H, s_hat, w, bits = orc.receive_frame(host[i].astype(np.complex128), s0, m, cp, d, qam)
+        assert np.array_equal(alone[i].bits[0].cpu().numpy(), bits)
+        assert rel(alone[i].s_hat[0].cpu().numpy(), s_hat) < REL_TOL
+        assert rel(alone[i].H[0].cpu().numpy(), H) < REL_TOL
+    for F in (3, 40):
+        xb = x.repeat((F + 1) // 2, 1, 1)[:F].contiguous()
+        out = P.receive_frames(xb, cfg, symbol0_offset=s0, n_data=d, latency=True)
+        torch.cuda.synchronize()
+        for j in range(F):
+            assert torch.equal(out.bits[j], alone[j % 2].bits[0])
+            assert torch.equal(out.s_hat[j], alone[j % 2].s_hat[0])
