@@ -51,7 +51,7 @@ def desc(**kw):
     (dict(qam_order=8), E.ConfigurationError),
     (dict(n_data=-1), E.ContractError),
     (dict(row_stride=100), E.ContractError),
-    (dict(options=4), E.ContractError),
+    (dict(options=8), E.ContractError),
     (dict(rx_samples=-1), E.ContractError),
 ])
 def test_check_desc_errors(lib, kw, exc):
