@@ -422,25 +422,62 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   };
   frame_sync();
 
+  // den = sum of the V lane partials in a fixed order.  V = NG groups of
+  // LPC_MAX consecutive lanes (fixed by the shape and plan, not by the CTA
+  // mapping): den = sum over groups (in group order) of the group's lane
+  // partials (in lane order).  With NG = 1 every owner sums the lanes itself;
+  // with NG > 1 (wide plans, spread over a cluster) the first lane of each
+  // group sums its group into gdenbuf first, so owners read NG group sums
+  // instead of V partials (distributed shared memory is slow to chase).
+  constexpr int GL = BC::LPC_MAX;
+  const int NG = V / GL;
+  float* gdenbuf = reinterpret_cast<float*>(smem_raw + BBAR + (size_t)lpc * M * 12);  // [M], one group per CTA
+  auto lane_den = [&](int q, float (&acc)[P]) {  // acc += lane q's partial (lane q lives in CTA q / lpc)
+    const uint32_t rk = (uint32_t)(q / lpc);
+    const float* src = denbuf + (q - (int)rk * lpc) * M + t;
+    if (rk == crank) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] += src[i * G];
+    } else {
+      const uint32_t ra = dsmem_addr(src, rk);
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] += ld_dsmem(ra + 4u * (uint32_t)(i * G));
+    }
+  };
+  if (NG > 1) {
+    if (v % GL == 0) {
+      float gs[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) gs[i] = 0.0f;
+      for (int q = v; q < v + GL; ++q) lane_den(q, gs);
+#pragma unroll
+      for (int i = 0; i < P; ++i) gdenbuf[i * G + t] = gs[i];
+    }
+    frame_sync();
+  }
+
   // the symbol owned by this lane: its first row lies in [r0, r1)
   const int d_own = has_rows ? (r0 + N - 1) / N : D;
   const bool owns = has_rows && d_own < D && d_own * N < r1;
   uint32_t flag = 0;
   if (owns || v == 0) {
-    // den = fixed-order sum of the V lane partials (lane q lives in CTA q / lpc)
     float den[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) den[i] = 0.0f;
-    for (int q = 0; q < V; ++q) {
-      const uint32_t rk = (uint32_t)(q / lpc);
-      const float* src = denbuf + (q - (int)rk * lpc) * M + t;
-      if (rk == crank) {
+    if (NG == 1) {
+      for (int q = 0; q < V; ++q) lane_den(q, den);
+    } else {
+      for (int c = 0; c < NG; ++c) {  // group c's sum lives in the CTA of its first lane
+        const uint32_t rk = (uint32_t)(c * GL / lpc);
+        const float* src = gdenbuf + t;
+        if (rk == crank) {
 #pragma unroll
-        for (int i = 0; i < P; ++i) den[i] += src[i * G];
-      } else {
-        const uint32_t ra = dsmem_addr(src, rk);
+          for (int i = 0; i < P; ++i) den[i] += src[i * G];
+        } else {
+          const uint32_t ra = dsmem_addr(src, rk);
 #pragma unroll
-        for (int i = 0; i < P; ++i) den[i] += ld_dsmem(ra + 4u * (uint32_t)(i * G));
+          for (int i = 0; i < P; ++i) den[i] += ld_dsmem(ra + 4u * (uint32_t)(i * G));
+        }
       }
     }
     if (v == 0) {

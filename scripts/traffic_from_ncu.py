@@ -21,7 +21,10 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 rd = d["dram__bytes_read.sum"][0] * scale[d["dram__bytes_read.sum"][1]]
 wr = d["dram__bytes_write.sum"][0] * scale[d["dram__bytes_write.sum"][1]]
 dur = d["gpu__time_duration.sum"][0] * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3}[d["gpu__time_duration.sum"][1]]
-out = {"dram_bytes_per_frame": (rd + wr) / frames, "dram_read_bytes": rd, "dram_write_bytes": wr,
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+import bench  # noqa: E402
+
+out = {"dram_bytes_per_frame": (rd + wr) / frames, "kernel_source_hash": bench.kernel_source_hash(), "dram_read_bytes": rd, "dram_write_bytes": wr,
        "frames_in_launch": frames, "ncu_duration_s": dur, "source": label,
        "note": "ncu --set full --clock-control none, one launch of the product kernel; writes still resident in L2 at "
                "kernel end are not counted by dram__bytes_write"}
