@@ -1,5 +1,6 @@
-// Balanced fused receive for M in {1024, 2048, 4096} (FFT lanes of G = 32,
-// 64, 128 threads, P = 32 points per thread): CP drop + FFT + fftshift -> LS
+// Balanced fused receive for M in {256, 512, 1024, 2048, 4096} (FFT lanes of
+// G = 16, 16, 32, 64, 128 threads; P = 16 or 32 points per thread; lanes
+// narrower than a warp run in pairs): CP drop + FFT + fftshift -> LS
 // -> MRC -> divide -> demap (receiver.py:238-267,308-348) with the work of a
 // frame cut into V "virtual lanes" whose arithmetic does not depend on how
 // the lanes are mapped onto CTAs.
@@ -41,18 +42,41 @@ constexpr size_t BBAR = 1024;   // mbarriers, TMEM address word, range table
 constexpr int BMAX_V = 96;      // workers per frame at most (8 CTAs x 12 lanes)
 constexpr int BMAX_CLUSTER = 8; // portable cluster size
 
+// A virtual lane is a whole number of warps.  FFT plans whose lanes are
+// narrower than a warp (G < 32: M = 64, 128, 256, 512) run RB = 32 / G FFTs
+// side by side in one warp: the warp streams "super-rows" of RB consecutive
+// antennas of one symbol (part b of the warp FFTs antenna n' RB + b), and the
+// RB per-part partial sums are combined in part order before the epilogue.
 template <int M>
 struct BalCfg {
   using PI = PlanInfo<M>;
-  static constexpr int P = PI::P, G = PI::G, LW = G / 32, SLOT = PI::SLOT;
-  static constexpr int ACC = 2 * P;             // floats per accumulator set
+  static constexpr int P = PI::P, G = PI::G, SLOT = PI::SLOT;
+  static constexpr int RB = G < 32 ? 32 / G : 1;  // rows per lane iteration
+  static constexpr int WT = G < 32 ? 32 : G;      // threads per virtual lane
+  static constexpr int LW = WT / 32;              // warps per virtual lane
+  static constexpr int ACC = 2 * P;               // floats per accumulator set
   static constexpr int COLS = (2 * ACC + P + 15) / 16 * 16;  // 2 sets + den partial, per warp (16-aligned)
-  static constexpr int LPC_MAX = BMAXW / LW;    // lanes per CTA at most
-  // P = 8 lanes are register-lean: two CTAs per SM (24 warps) hide more latency
+  static constexpr int LPC_MAX = BMAXW / LW;      // lanes per CTA at most
+  // register-lean lanes: two CTAs per SM (24 warps) hide more latency
   static constexpr int MIN_CTAS = P <= 8 ? 2 : 1;
-  static_assert((P == 32 || P == 16 || P == 8) && G >= 32, "balanced kernel: whole-warp lanes, 8..32 points");
-  static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * SLOT * sizeof(float2); }
+  static_assert((P == 32 || P == 16 || P == 8) && G * RB == WT, "balanced kernel: 8..32 points per thread");
+  static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * RB * SLOT * sizeof(float2); }
 };
+
+// sum over the RB parts of a warp of value x in part order (identical result
+// in every part: each part adds the same RB values in the same order)
+template <int RB, int G>
+__device__ __forceinline__ float parts_sum(float x) {
+  if constexpr (RB == 1) {
+    return x;
+  } else {
+    const int t = threadIdx.x & (G - 1);
+    float s = __shfl_sync(0xffffffffu, x, t);
+#pragma unroll
+    for (int b = 1; b < RB; ++b) s += __shfl_sync(0xffffffffu, x, t + b * G);
+    return s;
+  }
+}
 
 // sum_{a=0}^{x} floor(a / V) (0 for x < 0)
 __device__ __forceinline__ long long floor_sum(long long x, int V) {
@@ -134,14 +158,17 @@ template <int M, bool BPSK, bool ZF, bool PROF>
 __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_kernel(const FusedParams p) {
   using BC = BalCfg<M>;
   constexpr int P = BC::P, G = BC::G, LW = BC::LW, SS = BC::SLOT, ACC = BC::ACC, COLS = BC::COLS;
+  constexpr int RB = BC::RB, WT = BC::WT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lpc = blockDim.x / G;
-  const int l = threadIdx.x / G, t = threadIdx.x % G, w = threadIdx.x >> 5;
+  const int lpc = blockDim.x / WT;
+  const int l = threadIdx.x / WT, t = threadIdx.x % G, w = threadIdx.x >> 5;
+  const int part = (threadIdx.x % WT) / G;  // which of the RB FFTs of the lane (0 for whole-warp lanes)
   const uint32_t crank = cluster_ctarank();
   const int V = lpc * (int)cluster_nctarank();
   const int v = (int)crank * lpc + l;  // virtual lane of this thread
   const int f = (int)cluster_id_x();   // one cluster per frame
   const int N = p.n_ant, D = p.n_data;
+  const int Nr = N / RB;  // super-antennas (the plan requires RB | N)
   uint32_t reject = 0u;
   const long long sym0 = frame_sym0(p, f, M, &reject);
   if (reject != 0u) {  // not detected / out of range: the whole cluster leaves; flagged, no traffic
@@ -159,21 +186,21 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
 #else
   const bool one_cta = V == lpc;
 #endif
-  float2* slot_base = reinterpret_cast<float2*>(smem_raw + BBAR) + (size_t)l * 2 * SS;
-  const bool leader = t == 0;
+  float2* slot_base = reinterpret_cast<float2*>(smem_raw + BBAR) + (size_t)l * 2 * RB * SS;
+  const bool leader = (threadIdx.x % WT) == 0;  // issues the lane's copies, keeps its stage cycles
   auto lane_sync = [&]() {
     if constexpr (LW == 1) __syncwarp();
-    else named_bar_sync(1 + l, G);
+    else named_bar_sync(1 + l, WT);
   };
 
-  if (threadIdx.x < 2 * lpc) mbar_init(&rx_bar[threadIdx.x], 1);
+  if (threadIdx.x < 2 * lpc) mbar_init(&rx_bar[threadIdx.x], RB);
   if (prof && leader) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) cyc[s] = 0u;
   }
   if (threadIdx.x == 0) mbar_init(h_bar, blockDim.x);
   fence_mbar_init();
-  if (w == 0) build_range_table(lo_tab, N, D, V);
+  if (w == 0) build_range_table(lo_tab, Nr, D, V);
   const int nw = lpc * LW;
   uint32_t cols = 32;
   while (cols < (uint32_t)(((nw + 3) / 4) * COLS)) cols <<= 1;
@@ -187,14 +214,18 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   const float2* frame = p.rx + (long long)f * p.frame_stride + sym0 + p.cp;
   float2* Hf = p.H + (long long)f * N * M;
   auto row_addr = [&](int s, int n) { return frame + (long long)n * p.row_stride + (long long)s * (M + p.cp); };
-  auto issue_rx = [&](const float2* src, int st) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t start = a & ~uintptr_t(15);
-    const uint32_t bytes = (uint32_t)(((a + (uintptr_t)M * 8u + 15u) & ~uintptr_t(15)) - start);
-    uint64_t* bar = &rx_bar[2 * l + st];
-    mbar_arrive_expect_tx(bar, bytes);
-    tma_bulk_g2s(slot_base + (size_t)st * SS, reinterpret_cast<const void*>(start), bytes, bar,
-                 l2_evict_first_policy());
+  // super-row (symbol s, super-antenna nr): RB copies into the stage's RB sub-slots
+  auto issue_rx = [&](int s, int nr, int st) {
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(row_addr(s, nr * RB + b));
+      const uintptr_t start = a & ~uintptr_t(15);
+      const uint32_t bytes = (uint32_t)(((a + (uintptr_t)M * 8u + 15u) & ~uintptr_t(15)) - start);
+      uint64_t* bar = &rx_bar[2 * l + st];
+      mbar_arrive_expect_tx(bar, bytes);
+      tma_bulk_g2s(slot_base + (size_t)(st * RB + b) * SS, reinterpret_cast<const void*>(start), bytes, bar,
+                   l2_evict_first_policy());
+    }
   };
   // stage st = k & 1 is used at every other step, so its phase is (k >> 1) & 1
   auto wait_rx = [&](int kk) { mbar_wait_parity(&rx_bar[2 * l + (kk & 1)], (uint32_t)(kk >> 1) & 1u); };
@@ -229,10 +260,10 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   // in flight exceed it (C4: 148 x 4 MB).  Each accumulator set still sees
   // its antennas in ascending order: the arithmetic is that of the
   // symbol-major order.
-  const int d_first = r0 < r1 ? r0 / N : 0;
-  const int nA = r0 - d_first * N;
-  const bool two = r0 < r1 && r1 - 1 >= (d_first + 1) * N;
-  const int nB = two ? r1 - 1 - (d_first + 1) * N : -1;
+  const int d_first = r0 < r1 ? r0 / Nr : 0;
+  const int nA = r0 - d_first * Nr;
+  const bool two = r0 < r1 && r1 - 1 >= (d_first + 1) * Nr;
+  const int nB = two ? r1 - 1 - (d_first + 1) * Nr : -1;
   // first row: antenna 0 of set B if the lane has one, else antenna nA of A;
   // next row after (n, set): (n, B) if the current is A and n <= nB, else
   // antenna n + 1 (skipping the gap nB < n < nA), set A from nA on
@@ -251,17 +282,18 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   };
   const int nrows = r1 - r0;
   int k = 0;  // stage counter across both phases
-  if (leader && v < N) issue_rx(row_addr(0, v), 0);
+  if (leader && v < Nr) issue_rx(0, v, 0);
   float2 y[P];
-  for (int n = v; n < N; n += V, ++k) {
+  for (int nr = v; nr < Nr; nr += V, ++k) {
     const int st = k & 1;
-    float2* slot = slot_base + (size_t)st * SS;
+    const int n = nr * RB + part;  // this part's antenna
+    float2* slot = slot_base + (size_t)(st * RB + part) * SS;
     if (leader) {
-      if (n + V < N) issue_rx(row_addr(0, n + V), st ^ 1);
+      if (nr + V < Nr) issue_rx(0, nr + V, st ^ 1);
       else if (nrows > 0) {  // first data row of phase B
         int d0, n0;
         first_row(d0, n0);
-        issue_rx(row_addr(1 + d0, n0), st ^ 1);
+        issue_rx(1 + d0, n0, st ^ 1);
       }
     }
     uint32_t tc = prof ? sm_clock() : 0u;
@@ -298,10 +330,10 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
     tmem_st<P>(t_den, dp);
     if (prof && leader) cyc[kStageLs] += sm_clock() - tc;
   }
-  if (leader && v >= N && nrows > 0) {  // no pilot rows
+  if (leader && v >= Nr && nrows > 0) {  // no pilot rows
     int d0, n0;
     first_row(d0, n0);
-    issue_rx(row_addr(1 + d0, n0), k & 1);
+    issue_rx(1 + d0, n0, k & 1);
   }
   tmem_wait_st();
   // H rows of this lane are published; lanes of the frame acquire them
@@ -320,14 +352,15 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   bool h_acquired = false;
 
   // ---------------- phase B: this lane's data rows -------------------------
-  int d, n;  // current row
-  first_row(d, n);
+  int d, nr;  // current super-row
+  first_row(d, nr);
   for (int q = 0; q < nrows; ++q, ++k) {
     const int st = k & 1;
-    float2* slot = slot_base + (size_t)st * SS;
-    int dn = d, nn = n;  // next row
+    const int n = nr * RB + part;  // this part's antenna
+    float2* slot = slot_base + (size_t)(st * RB + part) * SS;
+    int dn = d, nn = nr;  // next super-row
     next_row(dn, nn);
-    if (leader && q + 1 < nrows) issue_rx(row_addr(1 + dn, nn), st ^ 1);
+    if (leader && q + 1 < nrows) issue_rx(1 + dn, nn, st ^ 1);
     uint32_t tc = prof ? sm_clock() : 0u;
     wait_rx(k);
     const int sh = (int)((reinterpret_cast<uintptr_t>(row_addr(1 + d, n)) >> 3) & 1);
@@ -359,14 +392,14 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       tmem_ld16(tacc + 16 * c, a);
       tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int i = 8 * c + q;
+      for (int e = 0; e < 8; ++e) {
+        const int i = 8 * c + e;
         const float2 h = hreg[i];
         const float2 yy = y[i];
         // conj(H) * Y = h.x * (y.x, y.y) + h.y * (y.y, -y.x)  (numba_backend.py:149-150)
-        const float2 m = upk(fma2(bc(h.y), pk(yy.y, -yy.x), fma2(bc(h.x), pk(yy), pk(a[2 * q], a[2 * q + 1]))));
-        a[2 * q] = m.x;
-        a[2 * q + 1] = m.y;
+        const float2 m = upk(fma2(bc(h.y), pk(yy.y, -yy.x), fma2(bc(h.x), pk(yy), pk(a[2 * e], a[2 * e + 1]))));
+        a[2 * e] = m.x;
+        a[2 * e + 1] = m.y;
       }
       tmem_st16(tacc + 16 * c, a);
     });
@@ -382,7 +415,7 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
     fence_proxy_async_smem();  // reads of this slot before its next TMA refill
     lane_sync();
     if (prof && leader) cyc[kStageMrc] += sm_clock() - tc;
-    d = dn, n = nn;
+    d = dn, nr = nn;
   }
   if (!h_acquired) h_acquire();
 
@@ -397,19 +430,27 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   float* denbuf = reinterpret_cast<float*>(smem_raw + BBAR);                          // [lpc][M]
   float2* partbuf = reinterpret_cast<float2*>(smem_raw + BBAR + (size_t)lpc * M * 4);  // [lpc][M]
   const bool has_rows = r0 < r1;
-  const bool continues = has_rows && (r0 % N) != 0;  // set 0 continues a symbol owned by an earlier lane
+  const bool continues = has_rows && (r0 % Nr) != 0;  // set 0 continues a symbol owned by an earlier lane
+  // a point of the lane's RB parts is stored by part (i mod RB)
+  auto mine = [&](int i) { return RB == 1 || (i % RB) == part; };
   {
     float dp[P];
     tmem_ld<P>(t_den, dp);
     tmem_wait_ld();
 #pragma unroll
-    for (int i = 0; i < P; ++i) denbuf[l * M + i * G + t] = dp[i];
+    for (int i = 0; i < P; ++i) {
+      const float x = parts_sum<RB, G>(dp[i]);
+      if (mine(i)) denbuf[l * M + i * G + t] = x;
+    }
     if (continues) {
       float a[ACC];
       tmem_ld<ACC>(tbase, a);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < P; ++i) partbuf[l * M + i * G + t] = make_float2(a[2 * i], a[2 * i + 1]);
+      for (int i = 0; i < P; ++i) {
+        const float2 x = make_float2(parts_sum<RB, G>(a[2 * i]), parts_sum<RB, G>(a[2 * i + 1]));
+        if (mine(i)) partbuf[l * M + i * G + t] = x;
+      }
     }
   }
   auto frame_sync = [&] {  // all lanes of the frame (CTA or cluster)
@@ -451,14 +492,15 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       for (int i = 0; i < P; ++i) gs[i] = 0.0f;
       for (int q = v; q < v + GL; ++q) lane_den(q, gs);
 #pragma unroll
-      for (int i = 0; i < P; ++i) gdenbuf[i * G + t] = gs[i];
+      for (int i = 0; i < P; ++i)
+        if (mine(i)) gdenbuf[i * G + t] = gs[i];
     }
     frame_sync();
   }
 
   // the symbol owned by this lane: its first row lies in [r0, r1)
-  const int d_own = has_rows ? (r0 + N - 1) / N : D;
-  const bool owns = has_rows && d_own < D && d_own * N < r1;
+  const int d_own = has_rows ? (r0 + Nr - 1) / Nr : D;
+  const bool owns = has_rows && d_own < D && d_own * Nr < r1;
   uint32_t flag = 0;
   if (owns || v == 0) {
     float den[P];
@@ -491,7 +533,8 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       if (wdst != nullptr) {
         float* wd = wdst + wrow * M + t;
 #pragma unroll
-        for (int i = 0; i < P; ++i) wd[shifted_bin<M>(i, 0)] = den[i];
+        for (int i = 0; i < P; ++i)
+          if (mine(i)) wd[shifted_bin<M>(i, 0)] = den[i];
       }
 #pragma unroll
       for (int i = 0; i < P; ++i) {
@@ -503,6 +546,8 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       float a[ACC];
       tmem_ld<ACC>(tbase + (uint32_t)((d_own - d_first) * ACC), a);
       tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < ACC; ++j) a[j] = parts_sum<RB, G>(a[j]);  // the lane's RB antenna parts, in order
       // add the partials of the following lanes that continue this symbol, in
       // lane order; lanes without rows are skipped (N < V leaves some empty)
       for (int q = v + 1; q < V; ++q) {
@@ -512,7 +557,7 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
         const int q0 = lo_tab[q], q1 = lo_tab[q + 1];
 #endif
         if (q0 >= q1) continue;
-        if (q0 / N != d_own || q0 % N == 0) break;
+        if (q0 / Nr != d_own || q0 % Nr == 0) break;
         const uint32_t rk = (uint32_t)(q / lpc);
         const float2* src = partbuf + (q - (int)rk * lpc) * M + t;
         if (rk == crank) {
@@ -539,6 +584,7 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
         uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
 #pragma unroll
         for (int i = 0; i < P; ++i) {
+          if (!mine(i)) continue;
           const float dd = fmaxf(den[i], p.eps);  // np.maximum(den, eps)
           const float2 shv = make_float2(a[2 * i] / dd, a[2 * i + 1] / dd);
           if (!isfinite(shv.x) || !isfinite(shv.y)) flag |= 1u;
@@ -554,6 +600,7 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
         }
 #pragma unroll
         for (int i = 0; i < P; ++i) {
+          if (!mine(i)) continue;
           if (!isfinite(a[2 * i]) || !isfinite(a[2 * i + 1])) flag |= 1u;
           ndst[shifted_bin<M>(i, 0)] = make_float2(a[2 * i], a[2 * i + 1]);
         }
@@ -583,7 +630,7 @@ cudaError_t launch_t(const FusedParams& p, const BalancedPlan& bp, cudaStream_t 
   if (cudaError_t e = ensure_smem_attr(kern, 227 * 1024, done); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.n_frames * (unsigned)bp.cluster, 1, 1);
-  cfg.blockDim = dim3((unsigned)(bp.lanes_per_cta * BC::G), 1, 1);
+  cfg.blockDim = dim3((unsigned)(bp.lanes_per_cta * BC::WT), 1, 1);
   // CTAs of one cluster may share an SM; every CTA allocates TMEM (blocking
   // tcgen05.alloc), so more co-resident CTAs than the SM's 512 columns hold
   // could wait forever on cluster-mates parked at a cluster barrier.  Pad the
@@ -627,6 +674,7 @@ bool plan_m(int n_ant, int n_data, int n_frames, int n_sm, bool latency, Balance
   // rows) never spans more than two symbols.  Few CTAs per frame keep the
   // cluster small at large batches (a GPC fits fewer 8-CTA clusters than its
   // SM count suggests, and the epilogue waits on every CTA of the frame).
+  if (n_ant % BC::RB != 0) return false;  // sub-warp FFT lanes pair up antennas
   int c = (n_data + 1 + LMAX - 1) / LMAX;
   if (latency) {  // OFDMRX_OPT_LATENCY: the widest portable cluster, >= ~4 rows per worker
     const long long rows = (long long)n_ant * (1 + n_data);
@@ -660,6 +708,7 @@ bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool la
   if (n_ant < 1 || n_data < 0) return false;
   switch (M) {
     case 256: return plan_m<256>(n_ant, n_data, n_frames, n_sm, latency, out);
+    case 512: return plan_m<512>(n_ant, n_data, n_frames, n_sm, latency, out);
     case 1024: return plan_m<1024>(n_ant, n_data, n_frames, n_sm, latency, out);
     case 2048: return plan_m<2048>(n_ant, n_data, n_frames, n_sm, latency, out);
     case 4096: return plan_m<4096>(n_ant, n_data, n_frames, n_sm, latency, out);
@@ -671,6 +720,7 @@ bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool la
 size_t balanced_smem_bytes(int M, int lanes_per_cta) {
   switch (M) {
     case 256: return BalCfg<256>::smem_bytes(lanes_per_cta);
+    case 512: return BalCfg<512>::smem_bytes(lanes_per_cta);
     case 1024: return BalCfg<1024>::smem_bytes(lanes_per_cta);
     case 2048: return BalCfg<2048>::smem_bytes(lanes_per_cta);
     case 4096: return BalCfg<4096>::smem_bytes(lanes_per_cta);
@@ -682,6 +732,7 @@ cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp,
   if (p.n_frames == 0) return cudaSuccess;
   switch (M) {
     case 256: return launch_m<256>(p, bp, s);
+    case 512: return launch_m<512>(p, bp, s);
     case 1024: return launch_m<1024>(p, bp, s);
     case 2048: return launch_m<2048>(p, bp, s);
     case 4096: return launch_m<4096>(p, bp, s);

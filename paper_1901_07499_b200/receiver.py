@@ -308,57 +308,97 @@ def _segments(slots):
     return segs
 
 
+class _SegmentStaging:
+    """Per-engine buffers of one pilot-led segment shape: a page-locked host
+    capture, its device copy, the device outputs and page-locked host
+    outputs.  Reused across segments, so a segment costs one host copy into
+    pinned memory, one H2D, one launch, one batch of D2H copies and ONE
+    synchronisation (no per-call pinning or allocation)."""
+
+    def __init__(self, cfg, n_sym, dev):
+        n, m, L = cfg.n_antennas, cfg.fft_len, cfg.symbol_len
+        d = n_sym - 1
+        qb = cfg.bits_per_qam_symbol
+        pin = dict(dtype=torch.complex64, pin_memory=True)
+        self.host_in = torch.empty((n, n_sym * L), **pin)
+        self.host_in_np = self.host_in.numpy()
+        self.dev_in = torch.empty((n, n_sym * L), dtype=torch.complex64, device=dev)
+        self.out = frames.allocate_outputs(1, n, m, d, cfg.qam_order, dev)
+        self.out.stage_cycles = torch.zeros((1, 5), dtype=torch.int64, device=dev)
+        self.h = torch.empty((n, m), **pin)
+        self.s_hat = torch.empty((max(d, 1), m), **pin)
+        self.w = torch.empty((m,), dtype=torch.float32, pin_memory=True)
+        self.bits = torch.empty((d * m * qb,), dtype=torch.uint8, pin_memory=True)
+        self.cyc = torch.empty((1, 5), dtype=torch.int64, pin_memory=True)
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+
+def _staging(engine, cfg, n_sym):
+    cache = engine.__dict__.setdefault("_staging_cache", {})
+    key = (cfg.n_antennas, cfg.fft_len, cfg.cp_len, cfg.qam_order, n_sym)
+    if key not in cache:
+        if len(cache) > 8:
+            cache.clear()
+        with torch.cuda.device(engine.device):
+            cache[key] = _SegmentStaging(cfg, n_sym, engine.device)
+    return cache[key]
+
+
 def _run_fused(slots, cfg, engine, pilot):
     """Each pilot-led segment is one fused launch; StageTimings per slot keep
     the reference's meaning (receiver.py:65-79, 245-266, 330-332):
-      read_s     getting the slot's samples onto the device: host staging of
-                 the segment plus its H2D copy (CUDA events), split by bytes;
+      read_s     getting the slot's samples onto the device: staging into the
+                 pinned capture plus its H2D copy (CUDA events), per slot;
       cp_drop_s  the host-side cp_drop / framing and finiteness checks;
       fft_s      the fused kernel's time in the slot's FFT (incl. sample wait);
       combine_s  ls (pilot) or mrc + demap (data), and the D2H of the results.
     The kernel's time is apportioned by ofdmrx_rx_frames_profiled's per-stage
     SM cycles (pilot FFT / LS / data FFT / MRC / combine+demap)."""
+    cfg = waveform.as_config(cfg)
     pilot = pilot or waveform.make_pilot(cfg.fft_len)
     estimate, symbols, timings = None, [], []
+    L = cfg.symbol_len
     for seg in _segments(slots):
         n_sym = len(seg)
         t0 = time.perf_counter()
-        for s in seg:
-            if np.atleast_2d(s.payload).shape[1] != cfg.symbol_len:
-                raise FramingError(
-                    f"symbol rows have {np.atleast_2d(s.payload).shape[1]} samples, expected {cfg.symbol_len}")
         payload = [np.atleast_2d(s.payload) for s in seg]
         for p in payload:
+            if p.shape[1] != L:
+                raise FramingError(f"symbol rows have {p.shape[1]} samples, expected {L}")
             if not np.all(np.isfinite(p[:, cfg.cp_len:])):
                 raise NumericInputError("non-finite samples entering the FFT stage")
         t1 = time.perf_counter()
-        capture = np.ascontiguousarray(np.concatenate(payload, axis=1), dtype=np.complex64)
+        st = _staging(engine, cfg, n_sym)
+        for i, p in enumerate(payload):  # c128 -> c64 straight into page-locked memory
+            st.host_in_np[:, i * L:(i + 1) * L] = p
+        t2 = time.perf_counter()
         with torch.cuda.device(engine.device):
-            host = torch.from_numpy(capture).pin_memory()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-            t2 = time.perf_counter()
+            ev = st.ev
             ev[0].record()
-            x = host.to(engine.device, non_blocking=True)
+            st.dev_in.copy_(st.host_in, non_blocking=True)
             ev[1].record()
-            out = frames.receive_frames(x, cfg, pilot, n_data=n_sym - 1, profile=True)
+            out = frames.receive_frames(st.dev_in, cfg, pilot, n_data=n_sym - 1, out=st.out, profile=True)
             ev[2].record()
-            H = out.H[0].cpu()
+            st.h.copy_(out.H[0], non_blocking=True)
             ev[3].record()
-            s_hat, w, bits = out.s_hat[0].cpu(), out.weights[0].cpu(), out.bits[0].cpu()
+            st.s_hat[:n_sym - 1].copy_(out.s_hat[0], non_blocking=True)
+            st.w.copy_(out.weights[0], non_blocking=True)
+            st.bits.copy_(out.bits[0], non_blocking=True)
+            st.cyc.copy_(out.stage_cycles, non_blocking=True)
             ev[4].record()
-            shares = out.stage_shares()
-            torch.cuda.synchronize()
+            ev[4].synchronize()
             h2d_s = ev[0].elapsed_time(ev[1]) * 1e-3
             kernel_s = ev[1].elapsed_time(ev[2]) * 1e-3
             d2h_h_s = ev[2].elapsed_time(ev[3]) * 1e-3
             d2h_s = ev[3].elapsed_time(ev[4]) * 1e-3
-        staging_s = t2 - t1
-        read = (staging_s + h2d_s) / n_sym
+        tot = st.cyc[0].double()
+        shares = (tot / max(float(tot.sum()), 1.0)).tolist()
+        read = (t2 - t1 + h2d_s) / n_sym
         cp = (t1 - t0) / n_sym
-        H = H.numpy().astype(np.complex128)
-        s_hat = s_hat.numpy().astype(np.complex128)
-        w = w.numpy().astype(np.float64)
-        bits = bits.numpy()
+        H = st.h.numpy().astype(np.complex128)
+        s_hat = st.s_hat.numpy().astype(np.complex128)
+        w = st.w.numpy().astype(np.float64)
+        bits = st.bits.numpy().copy()
         estimate = ChannelEstimate(gains=H, source_seq=seg[0].seq_no)
         timings.append(StageTimings(kind=PILOT, read_s=read, cp_drop_s=cp, fft_s=kernel_s * shares[0],
                                     combine_s=kernel_s * shares[1] + d2h_h_s))
