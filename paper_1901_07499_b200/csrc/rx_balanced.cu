@@ -1,6 +1,6 @@
-// Balanced fused receive for M in {256, 512, 1024, 2048, 4096} (FFT lanes of
-// G = 16, 16, 32, 64, 128 threads; P = 16 or 32 points per thread; lanes
-// narrower than a warp run in pairs): CP drop + FFT + fftshift -> LS
+// Balanced fused receive for M in {1024, 2048, 4096} (FFT lanes of G = 32,
+// 64, 128 threads, P = 32 points per thread; lanes narrower than a warp run
+// in pairs in the OFDMRX_BAL_PAIRED experiment build): CP drop + FFT + fftshift -> LS
 // -> MRC -> divide -> demap (receiver.py:238-267,308-348) with the work of a
 // frame cut into V "virtual lanes" whose arithmetic does not depend on how
 // the lanes are mapped onto CTAs.
@@ -58,7 +58,11 @@ struct BalCfg {
   static constexpr int COLS = (2 * ACC + P + 15) / 16 * 16;  // 2 sets + den partial, per warp (16-aligned)
   static constexpr int LPC_MAX = BMAXW / LW;      // lanes per CTA at most
   // register-lean lanes: two CTAs per SM (24 warps) hide more latency
+#ifdef OFDMRX_BAL_MINCTAS16
+  static constexpr int MIN_CTAS = P <= 16 ? 2 : 1;  // experiment: 85 registers at P = 16 (spills)
+#else
   static constexpr int MIN_CTAS = P <= 8 ? 2 : 1;
+#endif
   static_assert((P == 32 || P == 16 || P == 8) && G * RB == WT, "balanced kernel: 8..32 points per thread");
   static size_t smem_bytes(int lpc) { return BBAR + (size_t)lpc * 2 * RB * SLOT * sizeof(float2); }
 };
@@ -119,6 +123,10 @@ __device__ void build_range_table(int* lo, int N, int D, int V) {
   }
 }
 
+__device__ __forceinline__ void st_evict_last(float2* dst, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dst), "f"(v.x), "f"(v.y), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -282,14 +290,23 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   };
   const int nrows = r1 - r0;
   int k = 0;  // stage counter across both phases
-  if (leader && v < Nr) issue_rx(0, v, 0);
+  // this lane's pilot super-rows v, v + V, ... (pcount of them)
+  const int pcount = v < Nr ? (Nr - 1 - v) / V + 1 : 0;
+#ifdef OFDMRX_BAL_PILOT_DESC
+  // experiment: descending, so the H rows phase B reads first are the freshest in L2
+  const int pstart = v + (pcount - 1) * V, pstep = -V;
+#else
+  const int pstart = v, pstep = V;
+#endif
+  if (leader && pcount > 0) issue_rx(0, pstart, 0);
   float2 y[P];
-  for (int nr = v; nr < Nr; nr += V, ++k) {
+  for (int j = 0; j < pcount; ++j, ++k) {
+    const int nr = pstart + j * pstep;
     const int st = k & 1;
     const int n = nr * RB + part;  // this part's antenna
     float2* slot = slot_base + (size_t)(st * RB + part) * SS;
     if (leader) {
-      if (nr + V < Nr) issue_rx(0, nr + V, st ^ 1);
+      if (j + 1 < pcount) issue_rx(0, nr + pstep, st ^ 1);
       else if (nrows > 0) {  // first data row of phase B
         int d0, n0;
         first_row(d0, n0);
@@ -309,6 +326,10 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       tc = t1;
     }
     float2* hdst = Hf + (long long)n * M + t;
+#ifdef OFDMRX_BAL_H_EVICT_LAST
+    uint64_t hpol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(hpol));
+#endif
     float dp[P];
     tmem_wait_st();
     tmem_ld<P>(t_den, dp);
@@ -325,12 +346,16 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
         h = make_float2(fmaf(yy.y, pc.y, yy.x * pc.x), fmaf(-yy.x, pc.y, yy.y * pc.x));
       }
       dp[i] = fmaf(h.x, h.x, fmaf(h.y, h.y, dp[i]));
+#ifdef OFDMRX_BAL_H_EVICT_LAST
+      st_evict_last(hdst + shifted_bin<M>(i, 0), h, hpol);  // experiment: keep H in L2 for phase B
+#else
       hdst[shifted_bin<M>(i, 0)] = h;
+#endif
     }
     tmem_st<P>(t_den, dp);
     if (prof && leader) cyc[kStageLs] += sm_clock() - tc;
   }
-  if (leader && v >= Nr && nrows > 0) {  // no pilot rows
+  if (leader && pcount == 0 && nrows > 0) {  // no pilot rows
     int d0, n0;
     first_row(d0, n0);
     issue_rx(1 + d0, n0, k & 1);
@@ -707,8 +732,12 @@ bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool la
 #else
   if (n_ant < 1 || n_data < 0) return false;
   switch (M) {
+#ifdef OFDMRX_BAL_PAIRED
+    // experiment: paired sub-warp FFT lanes (A/B on one B200, C2 at 1000 /
+    // 2000 frames: 35 % / 37 % of the roofline vs 42 % / 51 % for rx_fused)
     case 256: return plan_m<256>(n_ant, n_data, n_frames, n_sm, latency, out);
     case 512: return plan_m<512>(n_ant, n_data, n_frames, n_sm, latency, out);
+#endif
     case 1024: return plan_m<1024>(n_ant, n_data, n_frames, n_sm, latency, out);
     case 2048: return plan_m<2048>(n_ant, n_data, n_frames, n_sm, latency, out);
     case 4096: return plan_m<4096>(n_ant, n_data, n_frames, n_sm, latency, out);
@@ -719,8 +748,10 @@ bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool la
 
 size_t balanced_smem_bytes(int M, int lanes_per_cta) {
   switch (M) {
+#ifdef OFDMRX_BAL_PAIRED
     case 256: return BalCfg<256>::smem_bytes(lanes_per_cta);
     case 512: return BalCfg<512>::smem_bytes(lanes_per_cta);
+#endif
     case 1024: return BalCfg<1024>::smem_bytes(lanes_per_cta);
     case 2048: return BalCfg<2048>::smem_bytes(lanes_per_cta);
     case 4096: return BalCfg<4096>::smem_bytes(lanes_per_cta);
@@ -731,8 +762,10 @@ size_t balanced_smem_bytes(int M, int lanes_per_cta) {
 cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp, cudaStream_t s) {
   if (p.n_frames == 0) return cudaSuccess;
   switch (M) {
+#ifdef OFDMRX_BAL_PAIRED
     case 256: return launch_m<256>(p, bp, s);
     case 512: return launch_m<512>(p, bp, s);
+#endif
     case 1024: return launch_m<1024>(p, bp, s);
     case 2048: return launch_m<2048>(p, bp, s);
     case 4096: return launch_m<4096>(p, bp, s);
