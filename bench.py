@@ -44,7 +44,7 @@ def frame_bytes(n, m, qam, d):
     return 8 * n * m * (1 + d) + 8 * n * m + 8 * m * d + b * m * d
 
 
-KERNEL_SOURCES = ("rx_balanced.cu", "rx_fused.cu", "ofdmrx_fft.cuh", "ofdmrx_internal.h", "capi.cu")
+KERNEL_SOURCES = ("rx_balanced.cu", "rx_fused.cu", "rx_latency.cu", "ofdmrx_fft.cuh", "ofdmrx_internal.h", "capi.cu")
 
 
 def kernel_source_hash():

@@ -95,13 +95,15 @@ typedef struct {
  * thread-block cluster instead of antenna shards). */
 #define OFDMRX_OPT_NO_SHARDS 2
 /* desc.options (ABI 2): latency plan for single frames and small batches
- * (the paper's per-symbol regime).  Each frame's work is cut
- * into the most workers a portable thread-block cluster holds (e.g. 96 for
- * C3 instead of 12), so one frame finishes ~8x sooner; throughput at large
- * batches is lower.  The antenna-sum order is fixed by (frame shape, this
- * option): results never depend on the batch size, and differ from the
- * default plan's only in fp32 rounding (bits bit-exact vs the reference in
- * every test).  ofdmrx_rx_plan reports the plan. */
+ * (the paper's per-symbol regime).  ofdmrx_rx_frames runs
+ * the row-parallel path: every FFT row of the batch is its own lane over the
+ * whole GPU, in three stream-ordered launches (pilot rows -> H; data rows ->
+ * conj(H) Y per antenna into scratch; combine over the antennas in ascending
+ * order = mrc_seq, divide, demap).  The partial-sum, peer-routed and detected
+ * entry points use the balanced kernel's widest plan (a whole portable
+ * cluster per frame) instead.  Results never depend on the batch size and
+ * differ from the default plan's only in fp32 rounding (bits bit-exact vs the
+ * reference in every test).  ofdmrx_rx_plan reports the plan. */
 #define OFDMRX_OPT_LATENCY 4
 
 OFDMRX_API int ofdmrx_abi_version(void);
@@ -123,6 +125,7 @@ OFDMRX_API int ofdmrx_check_desc(const ofdmrx_frame_desc* desc);
  */
 #define OFDMRX_KERNEL_BALANCED 1
 #define OFDMRX_KERNEL_FUSED 2
+#define OFDMRX_KERNEL_ROWS 3     /* OFDMRX_OPT_LATENCY, mode 0: row-parallel; workers = antennas */
 typedef struct {
   int32_t kernel;          /* OFDMRX_KERNEL_*                                  */
   int32_t workers;         /* balanced: virtual FFT lanes per frame; fused: 0  */

@@ -62,7 +62,7 @@ class Plan(ctypes.Structure):
                 ("kernel", "workers", "lanes_per_cta", "cluster", "ctas", "threads", "smem_bytes", "chunks")]
 
 
-KERNEL_BALANCED, KERNEL_FUSED = 1, 2
+KERNEL_BALANCED, KERNEL_FUSED, KERNEL_ROWS = 1, 2, 3
 
 
 _p = ctypes.c_void_p

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libofdmrx_b200.so")
-SOURCES = ["capi.cu", "rx_fused.cu", "rx_balanced.cu", "rx_staged.cu", "sync.cu", "synth.cu", "peer.cu"]
+SOURCES = ["capi.cu", "rx_fused.cu", "rx_balanced.cu", "rx_latency.cu", "rx_staged.cu", "sync.cu", "synth.cu", "peer.cu"]
 HEADERS = ["ofdmrx_fft.cuh", "ofdmrx_internal.h", "ofdmrx_twiddles.inc", "gen_twiddles.py",
            os.path.join("..", "..", "include", "ofdmrx_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

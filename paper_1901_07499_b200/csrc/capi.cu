@@ -147,13 +147,17 @@ struct Route {  // partial sums routed to the owners' peer inboxes
 // worker count, the fused kernel's chunking) depends on the frame shape only;
 // n_frames only changes how the work is mapped onto CTAs.
 struct RxPlan {
+  bool rows;  // row-parallel latency path
   bool balanced;
   ofdmrx::BalancedPlan bp;
   ofdmrx::FusedLaunch fl;
 };
 
-int make_plan(const ofdmrx_frame_desc* d, RxPlan* pl) {
+// rows_ok: the call can take the row-parallel path (mode 0, fixed symbol0, no routes)
+int make_plan(const ofdmrx_frame_desc* d, RxPlan* pl, bool rows_ok = false) {
   *pl = RxPlan{};
+  pl->rows = rows_ok && (d->options & OFDMRX_OPT_LATENCY) != 0;
+  if (pl->rows) return OFDMRX_OK;
   pl->balanced = ofdmrx::balanced_plan(d->fft_len, d->n_antennas, d->n_data, d->n_frames,
                                         ofdmrx::device_sm_count(), (d->options & OFDMRX_OPT_LATENCY) != 0,
                                         &pl->bp);
@@ -191,7 +195,7 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
     if (route->slot < 0) return fail(OFDMRX_ERR_CONTRACT, "slot must be >= 0");
   }
   RxPlan pl;
-  if (int rc = make_plan(d, &pl)) return rc;
+  if (int rc = make_plan(d, &pl, mode == 0 && route == nullptr && det == nullptr)) return rc;
   ofdmrx::FusedParams p{};
   p.rx = static_cast<const float2*>(rx);
   p.frame_stride = d->frame_stride;
@@ -240,6 +244,28 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
   }
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
+  if (pl.rows) {
+    void* hscratch = nullptr;
+    void* prod = nullptr;
+    if (p.H == nullptr) {
+      if (int rc = scratch_alloc(&hscratch, (size_t)d->n_frames * d->n_antennas * d->fft_len * 8, st)) return rc;
+      p.H = static_cast<float2*>(hscratch);
+    }
+    const size_t pb = ofdmrx::latency_scratch_bytes(d->n_frames, d->n_antennas, d->n_data, d->fft_len);
+    if (pb > 0) {
+      if (int rc = scratch_alloc(&prod, pb, st)) {
+        if (hscratch != nullptr) cudaFreeAsync(hscratch, st);
+        return rc;
+      }
+    }
+    e = ofdmrx::launch_latency(d->fft_len, p, static_cast<float2*>(prod), st);
+    cudaError_t e2 = prod != nullptr ? cudaFreeAsync(prod, st) : cudaSuccess;
+    cudaError_t e3 = hscratch != nullptr ? cudaFreeAsync(hscratch, st) : cudaSuccess;
+    if (e != cudaSuccess) return cuda_fail(e, "row-parallel receive launch");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "cudaFreeAsync");
+    return OFDMRX_OK;
+  }
   if (pl.balanced) {
     void* hscratch = nullptr;
     if (p.H == nullptr) {  // H travels through L2 between the phases: scratch when the caller wants none
@@ -370,9 +396,18 @@ int ofdmrx_rx_plan(const ofdmrx_frame_desc* desc, int32_t mode, int32_t zf, ofdm
   if (mode != 0 && mode != 1) return fail(OFDMRX_ERR_CONTRACT, "mode must be 0 or 1");
   (void)zf;  // the ZF output changes neither the kernel nor the order
   RxPlan pl;
-  if (int rc = make_plan(desc, &pl)) return rc;
+  if (int rc = make_plan(desc, &pl, mode == 0)) return rc;
   *out = ofdmrx_plan{};
-  if (pl.balanced) {
+  if (pl.rows) {
+    out->kernel = OFDMRX_KERNEL_ROWS;
+    out->workers = desc->n_antennas;
+    out->lanes_per_cta = 0;
+    out->cluster = 1;
+    out->ctas = 0;
+    out->threads = 256;
+    out->smem_bytes = 0;
+    out->chunks = 1;
+  } else if (pl.balanced) {
     out->kernel = OFDMRX_KERNEL_BALANCED;
     out->workers = pl.bp.workers;
     out->lanes_per_cta = pl.bp.lanes_per_cta;

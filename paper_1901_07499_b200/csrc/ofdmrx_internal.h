@@ -111,6 +111,12 @@ bool balanced_plan(int M, int n_ant, int n_data, int n_frames, int n_sm, bool la
 size_t balanced_smem_bytes(int M, int lanes_per_cta);
 cudaError_t launch_balanced(int M, const FusedParams& p, const BalancedPlan& bp, cudaStream_t s);
 
+// Row-parallel latency path (rx_latency.cu, OFDMRX_OPT_LATENCY, mode 0):
+// pilot rows -> H, data rows -> conj(H) Y into prod [F, D, N, M], combine.
+// Needs p.H (caller supplies scratch).
+size_t latency_scratch_bytes(int n_frames, int n_ant, int n_data, int M);
+cudaError_t launch_latency(int M, const FusedParams& p, float2* prod, cudaStream_t s);
+
 // multiprocessor count of the current device (cached per device)
 int device_sm_count();
 

@@ -123,10 +123,6 @@ __device__ void build_range_table(int* lo, int N, int D, int V) {
   }
 }
 
-__device__ __forceinline__ void st_evict_last(float2* dst, float2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dst), "f"(v.x), "f"(v.y), "l"(pol)
-               : "memory");
-}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -292,12 +288,7 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
   int k = 0;  // stage counter across both phases
   // this lane's pilot super-rows v, v + V, ... (pcount of them)
   const int pcount = v < Nr ? (Nr - 1 - v) / V + 1 : 0;
-#ifdef OFDMRX_BAL_PILOT_DESC
-  // experiment: descending, so the H rows phase B reads first are the freshest in L2
-  const int pstart = v + (pcount - 1) * V, pstep = -V;
-#else
   const int pstart = v, pstep = V;
-#endif
   if (leader && pcount > 0) issue_rx(0, pstart, 0);
   float2 y[P];
   for (int j = 0; j < pcount; ++j, ++k) {
@@ -326,10 +317,6 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       tc = t1;
     }
     float2* hdst = Hf + (long long)n * M + t;
-#ifdef OFDMRX_BAL_H_EVICT_LAST
-    uint64_t hpol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(hpol));
-#endif
     float dp[P];
     tmem_wait_st();
     tmem_ld<P>(t_den, dp);
@@ -346,11 +333,7 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
         h = make_float2(fmaf(yy.y, pc.y, yy.x * pc.x), fmaf(-yy.x, pc.y, yy.y * pc.x));
       }
       dp[i] = fmaf(h.x, h.x, fmaf(h.y, h.y, dp[i]));
-#ifdef OFDMRX_BAL_H_EVICT_LAST
-      st_evict_last(hdst + shifted_bin<M>(i, 0), h, hpol);  // experiment: keep H in L2 for phase B
-#else
       hdst[shifted_bin<M>(i, 0)] = h;
-#endif
     }
     tmem_st<P>(t_den, dp);
     if (prof && leader) cyc[kStageLs] += sm_clock() - tc;
@@ -411,11 +394,8 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
     }
     tmem_wait_st();
     // MAC in 16-column TMEM chunks: keeps y + hreg + one chunk in registers
-    static_for<ACC / 16>([&](auto ci) {
+    auto mac_chunk = [&](auto ci, float (&a)[16]) {
       constexpr int c = decltype(ci)::value;
-      float a[16];
-      tmem_ld16(tacc + 16 * c, a);
-      tmem_wait_ld();
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int i = 8 * c + e;
@@ -426,8 +406,24 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
         a[2 * e] = m.x;
         a[2 * e + 1] = m.y;
       }
-      tmem_st16(tacc + 16 * c, a);
-    });
+    };
+    // chunk c+1's TMEM load is in flight while chunk c is computed
+    {
+      constexpr int NCH = ACC / 16;
+      float a0[16], a1[16];
+      tmem_ld16(tacc, a0);
+      tmem_wait_ld();
+      static_for<NCH>([&](auto ci) {
+        constexpr int c = decltype(ci)::value;
+        float(&cur)[16] = (c & 1) ? a1 : a0;
+        float(&nxt)[16] = (c & 1) ? a0 : a1;
+        if constexpr (c + 1 < NCH) tmem_ld16(tacc + 16 * (c + 1), nxt);
+        mac_chunk(ci, cur);
+        tmem_st16(tacc + 16 * c, cur);
+        if constexpr (c + 1 < NCH) tmem_wait_ld();
+      });
+    }
+
     if constexpr (ZF) {  // per-antenna ZF output conj(H) Y / max(|H|^2, eps) (1-row mrc_combine)
       float2* zdst = p.zf + (((long long)f * D + d) * N + n) * M + t;
 #pragma unroll

@@ -7,7 +7,7 @@
 # Build the variant first (CPU is fine):
 #   python -m paper_1901_07499_b200.build --variant racecheck OFDMRX_RACECHECK_SERIAL
 mkdir -p gpurun_out/san
-CASES="balanced fused partials staged detect corr synth"
+CASES="balanced latency fused partials staged detect corr synth"
 for tool in memcheck synccheck initcheck racecheck; do
   for c in $CASES; do
     timeout 900 compute-sanitizer --tool $tool --print-limit 10 python scripts/sanitize_cases.py $c > gpurun_out/san/${tool}_${c}.log 2>&1

@@ -44,6 +44,17 @@ def balanced():
         torch.cuda.synchronize()
 
 
+def latency():
+    for (n, m, cp, qam, d, k) in ((64, 1024, 72, 16, 10, 2), (8, 64, 16, 4, 10, 3), (16, 2048, 256, 64, 3, 1)):
+        x, s0, cs = caps(m, cp, n, qam, d, k)
+        cfg = P.OfdmConfig(m, cp, n, qam_order=qam)
+        out = P.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, latency=True)
+        torch.cuda.synchronize()
+        check(out, cs, m, cp, d, qam, s0)
+        P.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, latency=True, zf=True, profile=True)
+        torch.cuda.synchronize()
+
+
 def fused():
     for (n, m, cp, qam, d, k) in ((8, 64, 16, 4, 10, 5), (16, 256, 32, 16, 10, 3), (3, 512, 64, 64, 20, 2)):
         x, s0, cs = caps(m, cp, n, qam, d, k)
@@ -107,7 +118,7 @@ def synth():
     torch.cuda.synchronize()
 
 
-CASES = {f.__name__: f for f in (balanced, fused, partials, staged, detect, corr, synth)}
+CASES = {f.__name__: f for f in (balanced, latency, fused, partials, staged, detect, corr, synth)}
 
 if __name__ == "__main__":
     torch.cuda.set_device(0)

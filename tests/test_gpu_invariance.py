@@ -130,9 +130,10 @@ def test_partials_independent_of_batch():
 @pytest.mark.parametrize("shape", [(64, 1024, 72, 16, 10), (16, 4096, 512, 16, 3), (256, 2048, 256, 64, 10)],
                          ids=["C3", "M4096", "C4"])
 def test_latency_plan(shape):
-    """OFDMRX_OPT_LATENCY (receive_frames(latency=True)): more workers per
-    frame than the throughput plan; bits exact vs the oracle, H / s_hat
-    within 1e-4; batch-invariant within the plan (F = 1, 3, 40)."""
+    """OFDMRX_OPT_LATENCY (receive_frames(latency=True)): the row-parallel
+    path (every FFT row its own lane, antenna sums ascending); bits exact vs
+    the oracle, H / s_hat / weights within 1e-4; batch-invariant within the
+    plan (F = 1, 3, 40); the ZF output and the stage attribution work."""
     import paper_1901_07499_b200 as P
     from paper_1901_07499_b200 import _lib, device
 
@@ -146,7 +147,10 @@ def test_latency_plan(shape):
     mk = lambda F, o: device.make_desc(F, n_ant, m, cp, d, qam, s0, x.shape[2], n_ant * x.shape[2],  # noqa: E731
                                        options=o, rx_samples=F * n_ant * x.shape[2])
     lat, thr = device.rx_plan(mk(1, opts | _lib.OPT_LATENCY)), device.rx_plan(mk(1, opts))
-    assert lat["workers"] > thr["workers"], (lat, thr)
+    assert lat["kernel"] == _lib.KERNEL_ROWS and lat["workers"] == n_ant, lat
+    # the partial-sum entry point takes the balanced kernel's widest plan instead
+    lat1 = device.rx_plan(mk(1, opts | _lib.OPT_LATENCY), mode=1)
+    assert lat1["kernel"] == _lib.KERNEL_BALANCED and lat1["workers"] > thr["workers"], (lat1, thr)
     alone = [P.receive_frames(x[i:i + 1], cfg, symbol0_offset=s0, n_data=d, latency=True) for i in range(2)]
     torch.cuda.synchronize()
     for i in range(2):
@@ -154,10 +158,21 @@ def test_latency_plan(shape):
         assert np.array_equal(alone[i].bits[0].cpu().numpy(), bits)
         assert rel(alone[i].s_hat[0].cpu().numpy(), s_hat) < REL_TOL
         assert rel(alone[i].H[0].cpu().numpy(), H) < REL_TOL
+        assert rel(alone[i].weights[0].cpu().numpy(), w) < REL_TOL
     for F in (3, 40):
         xb = x.repeat((F + 1) // 2, 1, 1)[:F].contiguous()
         out = P.receive_frames(xb, cfg, symbol0_offset=s0, n_data=d, latency=True)
         torch.cuda.synchronize()
+        assert int(out.flags.abs().sum()) == 0
         for j in range(F):
             assert torch.equal(out.bits[j], alone[j % 2].bits[0])
             assert torch.equal(out.s_hat[j], alone[j % 2].s_hat[0])
+            assert torch.equal(out.H[j], alone[j % 2].H[0])
+    z = P.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, latency=True, zf=True, profile=True)
+    torch.cuda.synchronize()
+    assert torch.equal(z.bits[0], alone[0].bits[0]) and (z.stage_cycles.cpu().numpy() > 0).all()
+    Hh = orc.receive_frame(host[0].astype(np.complex128), s0, m, cp, d, qam)[0]
+    for j in range(d):
+        lo = s0 + (j + 1) * (m + cp) + cp
+        Y = orc.freq_transform(host[0][:, lo:lo + m].astype(np.complex128))
+        assert rel(z.zf[0, j].cpu().numpy(), orc.zf_per_antenna(Y, Hh)) < REL_TOL
