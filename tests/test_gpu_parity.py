@@ -79,12 +79,15 @@ def test_fused_vs_oracle(P, case):
 GOLDEN_SETS = ["C1", "C1_0dB", "C2", "C3", "C3_0dB", "C4", "C4_0dB"]
 
 
-@pytest.mark.parametrize("tile", [1, 160], ids=["alone", "batch160"])
+@pytest.mark.parametrize("tile", [1, 160, "latency"], ids=["alone", "batch160", "latency_path"])
 @pytest.mark.parametrize("name", GOLDEN_SETS)
 def test_fused_vs_reference_golden(P, golden_dir, name, tile):
     """Directly against vectors produced by the reference itself, with the
-    frame received alone (F = 1, spread over a cluster for M >= 1024) and
-    tiled into a 160-frame batch (one CTA per frame: the benched mapping)."""
+    frame received alone (F = 1, spread over a cluster for M >= 1024),
+    tiled into a 160-frame batch (one CTA per frame: the benched mapping),
+    and alone through the row-parallel latency path (OFDMRX_OPT_LATENCY)."""
+    latency = tile == "latency"
+    tile = 1 if latency else tile
     g = dict(np.load(os.path.join(golden_dir, f"frames_{name}.npz")))
     n_ant, m, cp, qam, d = (int(v) for v in g["spec"])
     if tile > 1 and n_ant * m > 64 * 1024:
@@ -94,7 +97,7 @@ def test_fused_vs_reference_golden(P, golden_dir, name, tile):
         tag = f"f{int(f)}"
         streams, _, s0 = orc.synth_capture(m, cp, n_ant, qam, d, int(f), snr_db=float(g["snr_db"]))
         x = torch.from_numpy(streams.astype(np.complex64)).cuda()[None].repeat(tile, 1, 1).contiguous()
-        out = P.receive_frames(x, cfg, symbol0_offset=s0, n_data=d)
+        out = P.receive_frames(x, cfg, symbol0_offset=s0, n_data=d, latency=latency)
         torch.cuda.synchronize()
         if tile > 1:  # every copy identical, then check copy `tile - 1` below
             assert torch.equal(out.bits, out.bits[:1].expand_as(out.bits))
@@ -290,7 +293,7 @@ def test_large_batch_properties(P):
     assert ber < 1e-3
 
 
-@pytest.mark.parametrize("mode", ["gather", "allreduce"])
+@pytest.mark.parametrize("mode", ["gather", "allreduce", "scatter"])
 def test_antenna_sharded_receiver_world1(P, mode):
     """AntennaShardedReceiver through torch.distributed (NCCL, world size 1)."""
     import socket
