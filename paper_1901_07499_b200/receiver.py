@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import device, frames, waveform
+from . import _lib, device, frames, waveform
 from .errors import (
     ConfigurationError,
     ContractError,
@@ -330,6 +330,7 @@ class _SegmentStaging:
         self.w = torch.empty((m,), dtype=torch.float32, pin_memory=True)
         self.bits = torch.empty((d * m * qb,), dtype=torch.uint8, pin_memory=True)
         self.cyc = torch.empty((1, 5), dtype=torch.int64, pin_memory=True)
+        self.flags = torch.empty((1,), dtype=torch.int32, pin_memory=True)
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
 
@@ -365,12 +366,12 @@ def _run_fused(slots, cfg, engine, pilot):
         for p in payload:
             if p.shape[1] != L:
                 raise FramingError(f"symbol rows have {p.shape[1]} samples, expected {L}")
-            if not np.all(np.isfinite(p[:, cfg.cp_len:])):
-                raise NumericInputError("non-finite samples entering the FFT stage")
         t1 = time.perf_counter()
         st = _staging(engine, cfg, n_sym)
-        for i, p in enumerate(payload):  # c128 -> c64 straight into page-locked memory
-            st.host_in_np[:, i * L:(i + 1) * L] = p
+        for i, p in enumerate(payload):  # c128 -> c64 straight into page-locked memory (multithreaded copy)
+            src = torch.from_numpy(p) if p.dtype in (np.complex128, np.complex64) else torch.from_numpy(
+                p.astype(np.complex128))
+            st.host_in[:, i * L:(i + 1) * L].copy_(src)
         t2 = time.perf_counter()
         with torch.cuda.device(engine.device):
             ev = st.ev
@@ -385,12 +386,18 @@ def _run_fused(slots, cfg, engine, pilot):
             st.w.copy_(out.weights[0], non_blocking=True)
             st.bits.copy_(out.bits[0], non_blocking=True)
             st.cyc.copy_(out.stage_cycles, non_blocking=True)
+            st.flags.copy_(out.flags, non_blocking=True)
             ev[4].record()
             ev[4].synchronize()
             h2d_s = ev[0].elapsed_time(ev[1]) * 1e-3
             kernel_s = ev[1].elapsed_time(ev[2]) * 1e-3
             d2h_h_s = ev[2].elapsed_time(ev[3]) * 1e-3
             d2h_s = ev[3].elapsed_time(ev[4]) * 1e-3
+        # to_freq's finiteness check (receiver.py:202-203) on the device: a
+        # non-finite sample in any FFT window makes the frame's den / s_hat
+        # non-finite (OFDMRX_FLAG_NONFINITE) -- no host-side scan of the slots
+        if int(st.flags[0]) & _lib.FLAG_NONFINITE:
+            raise NumericInputError("non-finite samples entering the FFT stage")
         tot = st.cyc[0].double()
         shares = (tot / max(float(tot.sum()), 1.0)).tolist()
         read = (t2 - t1 + h2d_s) / n_sym

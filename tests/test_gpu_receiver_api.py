@@ -278,3 +278,32 @@ def test_fused_stage_attribution_covers_the_kernel(R):
         assert abs(sum(shares) - 1.0) < 1e-9
         # FFTs dominate: the data FFT share exceeds the MRC accumulation share
         assert shares[2] > shares[3]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["sequential", "b200"])
+def test_pipeline_nonfinite_samples(R, variant):
+    """to_freq's finiteness rule (receiver.py:202-203) through the fused
+    segment path: a NaN inside an FFT window raises NumericInputError (found
+    on the device, OFDMRX_FLAG_NONFINITE); a NaN inside a cyclic prefix is
+    never read and changes nothing."""
+    from paper_1901_07499_b200.errors import NumericInputError
+    from paper_1901_07499_b200.waveform import OfdmConfig, PilotDefinition
+
+    cfg = OfdmConfig(64, 16, 4, qam_order=4)
+    bits = np.random.default_rng(3).integers(0, 2, size=6 * 64 * 2, dtype=np.uint8)
+    pilot = orc.make_pilot(64)
+    samples, _, n_data = orc.build_frame_samples(64, 16, 4, pilot, bits, orc.generate_pn())
+    streams, _ = orc.apply_channel(samples, 4, mode="identity", rng_seed=3)
+    clean = R.run_ring_pipeline(R.extract_slots(_Cap(streams), _Det(255), cfg, 1 + n_data), cfg,
+                                R.make_engine(R.EngineKind(variant)), pilot=PilotDefinition(pilot))
+    cp_nan = streams.copy()
+    cp_nan[2, 255 + 2 * 80 + 3] = np.nan  # inside symbol 2's CP
+    res = R.run_ring_pipeline(R.extract_slots(_Cap(cp_nan), _Det(255), cfg, 1 + n_data), cfg,
+                              R.make_engine(R.EngineKind(variant)), pilot=PilotDefinition(pilot))
+    assert np.array_equal(res.bits, clean.bits)
+    win_nan = streams.copy()
+    win_nan[1, 255 + 3 * 80 + 16 + 5] = np.inf  # inside symbol 3's FFT window
+    with pytest.raises(NumericInputError):
+        R.run_ring_pipeline(R.extract_slots(_Cap(win_nan), _Det(255), cfg, 1 + n_data), cfg,
+                            R.make_engine(R.EngineKind(variant)), pilot=PilotDefinition(pilot))
