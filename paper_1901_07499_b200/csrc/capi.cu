@@ -251,14 +251,36 @@ int fused_common(const ofdmrx_frame_desc* d, const void* rx, const void* pilot, 
       if (int rc = scratch_alloc(&hscratch, (size_t)d->n_frames * d->n_antennas * d->fft_len * 8, st)) return rc;
       p.H = static_cast<float2*>(hscratch);
     }
-    const size_t pb = ofdmrx::latency_scratch_bytes(d->n_frames, d->n_antennas, d->n_data, d->fft_len);
-    if (pb > 0) {
-      if (int rc = scratch_alloc(&prod, pb, st)) {
+    // the per-antenna products of at most ~1 GB of frames at a time (the
+    // frames are independent: chunking changes no result)
+    const size_t per_frame = ofdmrx::latency_scratch_bytes(1, d->n_antennas, d->n_data, d->fft_len);
+    int chunk = d->n_frames;
+    if (per_frame > 0 && (size_t)chunk * per_frame > (1ull << 30)) {
+      chunk = (int)((1ull << 30) / per_frame);
+      if (chunk < 1) chunk = 1;
+    }
+    if (per_frame > 0) {
+      if (int rc = scratch_alloc(&prod, (size_t)chunk * per_frame, st)) {
         if (hscratch != nullptr) cudaFreeAsync(hscratch, st);
         return rc;
       }
     }
-    e = ofdmrx::launch_latency(d->fft_len, p, static_cast<float2*>(prod), st);
+    e = cudaSuccess;
+    for (int f0 = 0; f0 < d->n_frames && e == cudaSuccess; f0 += chunk) {
+      ofdmrx::FusedParams q = p;
+      const int fc = d->n_frames - f0 < chunk ? d->n_frames - f0 : chunk;
+      const long long M = d->fft_len, D = d->n_data, N = d->n_antennas;
+      q.n_frames = fc;
+      q.rx = p.rx + (long long)f0 * d->frame_stride;
+      q.H = p.H + (long long)f0 * N * M;
+      q.s_hat = p.s_hat != nullptr ? p.s_hat + (long long)f0 * D * M : nullptr;
+      q.weights = p.weights != nullptr ? p.weights + (long long)f0 * M : nullptr;
+      q.bits = p.bits != nullptr ? p.bits + (long long)f0 * D * M * p.qb : nullptr;
+      q.zf = p.zf != nullptr ? p.zf + (long long)f0 * D * N * M : nullptr;
+      q.flags = p.flags != nullptr ? p.flags + f0 : nullptr;
+      q.stage_cycles = p.stage_cycles != nullptr ? p.stage_cycles + (long long)f0 * ofdmrx::kStages : nullptr;
+      e = ofdmrx::launch_latency(d->fft_len, q, static_cast<float2*>(prod), st);
+    }
     cudaError_t e2 = prod != nullptr ? cudaFreeAsync(prod, st) : cudaSuccess;
     cudaError_t e3 = hscratch != nullptr ? cudaFreeAsync(hscratch, st) : cudaSuccess;
     if (e != cudaSuccess) return cuda_fail(e, "row-parallel receive launch");

@@ -414,7 +414,10 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
     atomicAdd(sc + (is_pilot ? kStageLs : kStageMrc), (unsigned long long)c_comb);
     atomicAdd(sc + kStageDemap, (unsigned long long)(sm_clock() - t_epi));
   }
-  if (p.num_dst != nullptr) __threadfence_system();  // peer stores before the exchange flags
+  if (p.num_dst != nullptr) {  // peer stores before the exchange flags: the CTA's
+    __syncthreads();            // stores happen-before thread 0's (cumulative) system fence
+    if (threadIdx.x == 0) __threadfence_system();
+  }
 }
 
 template <int M>
