@@ -309,22 +309,24 @@ def _segments(slots):
 
 
 class _SegmentStaging:
-    """Per-engine buffers of one pilot-led segment shape: a page-locked host
-    capture, its device copy, the device outputs and page-locked host
-    outputs.  Reused across segments, so a segment costs one host copy into
-    pinned memory, one H2D, one launch, one batch of D2H copies and ONE
-    synchronisation (no per-call pinning or allocation)."""
+    """Per-engine buffers of one pilot-led segment shape (and pilot): a
+    page-locked host capture, its device copy, the device outputs and
+    page-locked host outputs.  The device work of a segment (the
+    single-frame latency path of ofdmrx_rx_frames, then the D2H copies) is
+    captured once as two CUDA graphs and replayed between timing events, so a
+    segment costs one host copy into pinned memory, an H2D, two graph
+    launches and ONE synchronisation (no per-call pinning, allocation or
+    Python launch path)."""
 
-    def __init__(self, cfg, n_sym, dev):
+    def __init__(self, cfg, n_sym, dev, pilot):
         n, m, L = cfg.n_antennas, cfg.fft_len, cfg.symbol_len
         d = n_sym - 1
         qb = cfg.bits_per_qam_symbol
         pin = dict(dtype=torch.complex64, pin_memory=True)
+        self.cfg, self.n_sym, self.dev, self.pilot = cfg, n_sym, dev, pilot
         self.host_in = torch.empty((n, n_sym * L), **pin)
-        self.host_in_np = self.host_in.numpy()
         self.dev_in = torch.empty((n, n_sym * L), dtype=torch.complex64, device=dev)
         self.out = frames.allocate_outputs(1, n, m, d, cfg.qam_order, dev)
-        self.out.stage_cycles = torch.zeros((1, 5), dtype=torch.int64, device=dev)
         self.h = torch.empty((n, m), **pin)
         self.s_hat = torch.empty((max(d, 1), m), **pin)
         self.w = torch.empty((m,), dtype=torch.float32, pin_memory=True)
@@ -332,16 +334,71 @@ class _SegmentStaging:
         self.cyc = torch.empty((1, 5), dtype=torch.int64, pin_memory=True)
         self.flags = torch.empty((1,), dtype=torch.int32, pin_memory=True)
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        self.res = None
+        self.graph = None
+        self.calls = 0
+
+    def _kernel(self):
+        self.res = frames.receive_frames(self.dev_in, self.cfg, self.pilot, n_data=self.n_sym - 1, out=self.out,
+                                         profile=True, latency=True)
+
+    def _d2h(self):
+        out, d = self.res, self.n_sym - 1
+        self.h.copy_(out.H[0], non_blocking=True)
+        self.s_hat[:d].copy_(out.s_hat[0], non_blocking=True)
+        self.w.copy_(out.weights[0], non_blocking=True)
+        self.bits.copy_(out.bits[0], non_blocking=True)
+        self.cyc.copy_(out.stage_cycles, non_blocking=True)
+        self.flags.copy_(out.flags, non_blocking=True)
+
+    def _capture(self, fn):
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        return g
+
+    def run(self):
+        """The segment's device work; returns (h2d_s, kernel_s, d2h_h_s, d2h_s)
+        from CUDA events recorded between the (replayed) pieces."""
+        self.calls += 1
+        if self.graph is None and self.calls >= 2:  # first call eager (warm-up), then capture once
+            try:
+                self.graph = (self._capture(self._kernel), self._capture(self._d2h))
+            except Exception:  # noqa: BLE001 -- capture unsupported here: stay eager
+                self.graph = False
+                torch.cuda.synchronize()
+        ev = self.ev
+        ev[0].record()
+        self.dev_in.copy_(self.host_in, non_blocking=True)
+        ev[1].record()
+        if self.graph:
+            self.graph[0].replay()
+        else:
+            self._kernel()
+        ev[2].record()
+        if self.graph:
+            self.graph[1].replay()
+        else:
+            self._d2h()
+        ev[4].record()
+        ev[4].synchronize()
+        return (ev[0].elapsed_time(ev[1]) * 1e-3, ev[1].elapsed_time(ev[2]) * 1e-3, 0.0,
+                ev[2].elapsed_time(ev[4]) * 1e-3)
 
 
-def _staging(engine, cfg, n_sym):
+def _staging(engine, cfg, n_sym, pilot):
     cache = engine.__dict__.setdefault("_staging_cache", {})
-    key = (cfg.n_antennas, cfg.fft_len, cfg.cp_len, cfg.qam_order, n_sym)
+    pv = np.ascontiguousarray(getattr(pilot, "values", pilot))
+    key = (cfg.n_antennas, cfg.fft_len, cfg.cp_len, cfg.qam_order, n_sym, pv.tobytes())
     if key not in cache:
         if len(cache) > 8:
             cache.clear()
         with torch.cuda.device(engine.device):
-            cache[key] = _SegmentStaging(cfg, n_sym, engine.device)
+            cache[key] = _SegmentStaging(cfg, n_sym, engine.device, pilot)
     return cache[key]
 
 
@@ -367,32 +424,14 @@ def _run_fused(slots, cfg, engine, pilot):
             if p.shape[1] != L:
                 raise FramingError(f"symbol rows have {p.shape[1]} samples, expected {L}")
         t1 = time.perf_counter()
-        st = _staging(engine, cfg, n_sym)
+        st = _staging(engine, cfg, n_sym, pilot)
         for i, p in enumerate(payload):  # c128 -> c64 straight into page-locked memory (multithreaded copy)
             src = torch.from_numpy(p) if p.dtype in (np.complex128, np.complex64) else torch.from_numpy(
                 p.astype(np.complex128))
             st.host_in[:, i * L:(i + 1) * L].copy_(src)
         t2 = time.perf_counter()
         with torch.cuda.device(engine.device):
-            ev = st.ev
-            ev[0].record()
-            st.dev_in.copy_(st.host_in, non_blocking=True)
-            ev[1].record()
-            out = frames.receive_frames(st.dev_in, cfg, pilot, n_data=n_sym - 1, out=st.out, profile=True)
-            ev[2].record()
-            st.h.copy_(out.H[0], non_blocking=True)
-            ev[3].record()
-            st.s_hat[:n_sym - 1].copy_(out.s_hat[0], non_blocking=True)
-            st.w.copy_(out.weights[0], non_blocking=True)
-            st.bits.copy_(out.bits[0], non_blocking=True)
-            st.cyc.copy_(out.stage_cycles, non_blocking=True)
-            st.flags.copy_(out.flags, non_blocking=True)
-            ev[4].record()
-            ev[4].synchronize()
-            h2d_s = ev[0].elapsed_time(ev[1]) * 1e-3
-            kernel_s = ev[1].elapsed_time(ev[2]) * 1e-3
-            d2h_h_s = ev[2].elapsed_time(ev[3]) * 1e-3
-            d2h_s = ev[3].elapsed_time(ev[4]) * 1e-3
+            h2d_s, kernel_s, d2h_h_s, d2h_s = st.run()
         # to_freq's finiteness check (receiver.py:202-203) on the device: a
         # non-finite sample in any FFT window makes the frame's den / s_hat
         # non-finite (OFDMRX_FLAG_NONFINITE) -- no host-side scan of the slots
