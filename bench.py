@@ -708,6 +708,7 @@ def run_latency(args):
         gts.sort()
         k_us, _ = graph_time_us(kernel)
         k_tp_us, _ = graph_time_us(lambda: kernel(False))
+        h2d_us, _ = graph_time_us(lambda: dev_x.copy_(host, non_blocking=True))
         prof = frames.receive_frames(dev_x, cfg, symbol0_offset=s0, n_data=d, profile=True, latency=True)
         torch.cuda.synchronize()
         shares = prof.stage_shares()
@@ -719,6 +720,7 @@ def run_latency(args):
             "h2d_bytes": int(host.numel() * 8), "d2h_bytes": int(bits_host.numel()),
             "api_us_per_frame": {"median": med, "p99": p99}, "api_us_per_symbol": med / sym,
             "graph_us_per_frame": gmed, "graph_us_per_symbol": gmed / sym,
+            "h2d_alone_us": h2d_us,
             "kernel_us_per_frame": k_us, "kernel_us_per_symbol": k_us / sym,
             "kernel_us_per_frame_throughput_plan": k_tp_us,
             "kernel_stage_us_per_symbol": {
