@@ -88,21 +88,44 @@ __global__ void __launch_bounds__(kLatThreads) lat_rows_kernel(const FusedParams
   }
 }
 
-// CTA = (frame, 32 subcarriers) x up to 16 warps.  Warp 0 sums den over the
-// antennas (ascending) and shares it through shared memory; warp w then
-// combines data symbols d = w, w + 16, ...: num over the antennas
-// (ascending), divide, demap.  32 loads in flight per thread.
+// CTA = (frame, 32 subcarriers) x (nw + 1) warps: warps 0..nw-1 sum the
+// products of data symbols d = w, w + nw, ... over the antennas while warp
+// nw sums den (both in ascending antenna order, 32 loads in flight per
+// thread), so the L2 round trips of num and den overlap; then divide, demap.
 constexpr int kCombWarps = 16;
+__device__ __forceinline__ float2 sum_rows(const float2* src, int N, int M, bool ok) {
+  float2 acc = make_float2(0.f, 0.f);
+  for (int n0 = 0; n0 < N; n0 += 32) {
+    float2 v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = ok && n0 + e < N ? __ldcg(src + (long long)(n0 + e) * M) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (n0 + e < N) acc = upk(add2(pk(acc), pk(v[e])));
+  }
+  return acc;
+}
+
 template <bool PROF>
-__global__ void __launch_bounds__(32 * kCombWarps) lat_combine_kernel(const FusedParams p, const float2* prod, int M) {
+__global__ void __launch_bounds__(32 * (kCombWarps + 1)) lat_combine_kernel(const FusedParams p, const float2* prod,
+                                                                             int M) {
   __shared__ float den_s[32];
   const int N = p.n_ant, D = p.n_data;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x >> 5) - 1;
   const int f = blockIdx.x, k = blockIdx.y * 32 + lane;
   const bool ok = k < M;
   const uint32_t c0 = PROF ? sm_clock() : 0u;
   uint32_t flag = 0;
-  if (w == 0) {
+  const QamParams qp{p.qb, p.levels, p.qscale};
+  auto finish = [&](int d, float2 num, float dd) {
+    const float2 sh = make_float2(num.x / dd, num.y / dd);
+    if (!isfinite(sh.x) || !isfinite(sh.y)) flag |= 1u;
+    const long long sym = ((long long)f * D + d) * M + k;
+    p.s_hat[sym] = sh;
+    demap_store(sh, qp, p.bits + sym * p.qb);
+  };
+  float2 num0 = make_float2(0.f, 0.f);
+  if (w == nw) {  // den warp
     const float2* H = p.H + (long long)f * N * M + k;
     float den = 0.0f;
     for (int n0 = 0; n0 < N; n0 += 32) {
@@ -119,25 +142,14 @@ __global__ void __launch_bounds__(32 * kCombWarps) lat_combine_kernel(const Fuse
       if (den < p.eps) flag |= 2u;
       if (p.weights != nullptr) p.weights[(long long)f * M + k] = den;
     }
+  } else if (w < D) {  // this warp's first symbol, concurrently with den
+    num0 = sum_rows(prod + ((long long)f * D + w) * N * M + k, N, M, ok);
   }
   __syncthreads();
   const float dd = fmaxf(den_s[lane], p.eps);  // np.maximum(den, eps)
-  for (int d = w; d < D && ok; d += nw) {
-    const float2* pr = prod + ((long long)f * D + d) * N * M + k;
-    float2 num = make_float2(0.f, 0.f);
-    for (int n0 = 0; n0 < N; n0 += 32) {
-      float2 v[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = n0 + e < N ? __ldcg(pr + (long long)(n0 + e) * M) : make_float2(0.f, 0.f);
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (n0 + e < N) num = upk(add2(pk(num), pk(v[e])));
-    }
-    const float2 sh = make_float2(num.x / dd, num.y / dd);
-    if (!isfinite(sh.x) || !isfinite(sh.y)) flag |= 1u;
-    const long long sym = ((long long)f * D + d) * M + k;
-    p.s_hat[sym] = sh;
-    demap_store(sh, QamParams{p.qb, p.levels, p.qscale}, p.bits + sym * p.qb);
+  if (w < nw && ok) {
+    if (w < D) finish(w, num0, dd);
+    for (int d = w + nw; d < D; d += nw) finish(d, sum_rows(prod + ((long long)f * D + d) * N * M + k, N, M, ok), dd);
   }
   if (flag != 0u && p.flags != nullptr) atomicOr(&p.flags[f], flag);
   if (PROF && lane == 0)  // per warp, like the row kernels' per-lane attribution
@@ -163,7 +175,8 @@ cudaError_t launch_all(const FusedParams& p, float2* prod, cudaStream_t s) {
   if (cudaError_t e = launch_rows<M, true, BPSK, false, PROF>(p, prod, s); e != cudaSuccess) return e;
   if (cudaError_t e = launch_rows<M, false, BPSK, ZF, PROF>(p, prod, s); e != cudaSuccess) return e;
   const int nw = p.n_data < 1 ? 1 : (p.n_data < kCombWarps ? p.n_data : kCombWarps);
-  lat_combine_kernel<PROF><<<dim3((unsigned)p.n_frames, (unsigned)((M + 31) / 32)), 32 * nw, 0, s>>>(p, prod, M);
+  lat_combine_kernel<PROF><<<dim3((unsigned)p.n_frames, (unsigned)((M + 31) / 32)), 32 * (nw + 1), 0, s>>>(p, prod,
+                                                                                                          M);
   return cudaGetLastError();
 }
 

@@ -8,7 +8,10 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
-from paper_1901_07499_b200 import frames  # noqa: E402
+from paper_1901_07499_b200 import _lib, frames  # noqa: E402
+
+if os.environ.get("OFDMRX_VARIANT_LIB"):  # experiment build; the package itself never does this
+    _lib.LIB_PATH = os.environ["OFDMRX_VARIANT_LIB"]
 
 for name in sys.argv[1:] or ["C3", "C1"]:
     n, m, cp, qam, d, _ = bench.CONFIGS[name]
