@@ -1,9 +1,10 @@
 """Randomised parity sweep of ofdmrx_rx_frames against the oracle: FFT sizes
 2..4096, 1..70 antennas, 0..14 data symbols, every QAM order, random CP,
-symbol0 offsets (odd sample offsets included), padded rows and ZF on/off,
-so every kernel path (rx_balanced at any cluster mapping, rx_fused) meets
-the same bar: bits exact, H / s_hat / weights within
-1e-4 relative.  Fixed seed: the same 36 configurations every run."""
+symbol0 offsets (odd sample offsets included), padded rows, ZF on/off and
+the throughput / single-frame latency plans, so every kernel path
+(rx_balanced at any cluster mapping, rx_fused, the row-parallel latency
+path) meets the same bar: bits exact, H / s_hat / weights within 1e-4
+relative.  Fixed seed: the same 60 configurations every run."""
 
 import math
 
@@ -25,7 +26,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def _configs(n=36, seed=20261017):
+def _configs(n=60, seed=20261017):
     rng = np.random.default_rng(seed)
     out = []
     while len(out) < n:
@@ -43,11 +44,12 @@ def _configs(n=36, seed=20261017):
     return out
 
 
-@pytest.mark.parametrize("cfg", _configs(), ids=lambda c: f"M{c[0]}N{c[1]}D{c[2]}q{c[3]}cp{c[4]}F{c[5]}")
+@pytest.mark.parametrize("cfg", _configs(),
+                         ids=lambda c: f"M{c[0]}N{c[1]}D{c[2]}q{c[3]}cp{c[4]}F{c[5]}{'lat' if c[9] else ''}")
 def test_fuzz_fused_vs_oracle(cfg):
     import paper_1901_07499_b200 as P
 
-    m, n_ant, d, qam, cp, nf, off, pad, zf, shards, seed = cfg
+    m, n_ant, d, qam, cp, nf, off, pad, zf, latency, seed = cfg
     rng = np.random.default_rng(seed)
     b = int(math.log2(qam))
     pilot = orc.make_pilot(m)
@@ -63,7 +65,7 @@ def test_fuzz_fused_vs_oracle(cfg):
         streams[f, :, off:off + st.shape[1]] = st
     cfgp = P.OfdmConfig(m, cp, n_ant, qam_order=qam)
     x = torch.from_numpy(streams.astype(np.complex64)).cuda()
-    out = P.receive_frames(x, cfgp, symbol0_offset=off + 255, n_data=d, zf=zf, shards=shards)
+    out = P.receive_frames(x, cfgp, symbol0_offset=off + 255, n_data=d, zf=zf, latency=latency)
     torch.cuda.synchronize()
     assert int((out.flags & 1).sum()) == 0
     for f in range(nf):
