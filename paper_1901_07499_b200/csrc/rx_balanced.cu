@@ -506,6 +506,18 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       for (int i = 0; i < P; ++i) acc[i] += ld_dsmem(ra + 4u * (uint32_t)(i * G));
     }
   };
+  // one-CTA frames: the whole CTA sums den once (each thread a strided set of
+  // subcarriers, lanes in order), instead of every owner summing all V
+  // partials itself
+  const bool coop_den = one_cta && NG == 1;
+  if (coop_den) {
+    for (int k2 = threadIdx.x; k2 < M; k2 += blockDim.x) {
+      float acc = 0.0f;
+      for (int q = 0; q < V; ++q) acc += denbuf[q * M + k2];
+      gdenbuf[k2] = acc;
+    }
+    __syncthreads();
+  }
   if (NG > 1) {
     if (v % GL == 0) {
       float gs[P];
@@ -527,7 +539,10 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
     float den[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) den[i] = 0.0f;
-    if (NG == 1) {
+    if (coop_den) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) den[i] = gdenbuf[i * G + t];
+    } else if (NG == 1) {
       for (int q = 0; q < V; ++q) lane_den(q, den);
     } else {
       for (int c = 0; c < NG; ++c) {  // group c's sum lives in the CTA of its first lane
