@@ -430,23 +430,19 @@ static cudaError_t plan_impl(int n_frames, int n_data, FusedLaunch* l) {
   if (FC::smem_bytes(1, 1 + (n_data > 0 ? 1 : 0)) > smem_cap) return cudaErrorInvalidValue;
   // two pilot units (alternating antennas) keep the LS estimate off the critical
   // path when there are enough data units to feed
-  int npilot = 2;
+  // one pilot unit: it is as busy as a data unit (one antenna row per step)
+  // and the 2-deep H ring keeps it ahead (A/B on one B200: two alternating
+  // pilot units were 1.6 points slower at C1 and equal at C2)
+  const int npilot = 1;
   int dc_cap = units_max - npilot;
   if (dc_cap > 15) dc_cap = 15;
   while (dc_cap > 1 && FC::smem_bytes(1, npilot + dc_cap) > smem_cap) --dc_cap;
-  if (dc_cap < 4) {
-    npilot = 1;
-    dc_cap = units_max - 1;
-    if (dc_cap > 15) dc_cap = 15;
-    while (dc_cap > 1 && FC::smem_bytes(1, 1 + dc_cap) > smem_cap) --dc_cap;
-  }
   int dc = 0, chunks = 1;
   if (n_data > 0) {
     dc = n_data < dc_cap ? n_data : dc_cap;
     chunks = (n_data + dc - 1) / dc;
     dc = (n_data + chunks - 1) / chunks;
   }
-  if (dc < 4) npilot = 1;
   const int per_group = npilot + dc;
   int ngroups = units_max / per_group;
   if (ngroups < 1) ngroups = 1;
