@@ -43,7 +43,7 @@ struct FusedCfg {
   static size_t smem_bytes(int ngroups, int per_group) {
     const int units = ngroups * per_group, lanes = units * GI;
     return bar_bytes(lanes, ngroups) + (size_t)NSTAGE * lanes * SLOT_STRIDE * 8 +
-           (size_t)ngroups * RING * GI * HSTRIDE * 8;
+           (size_t)ngroups * RING * GI * HSTRIDE * 8 + (size_t)ngroups * GI * M * 4;  // + den per item
   }
   // TMEM columns: warps of a lane quarter (warp % 4) stack 2P columns each
   __host__ __device__ static uint32_t tmem_cols(int nwarps) {
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   constexpr int NACC = 2 * P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
-  const int npilot = p.npilot;          // pilot units per group (alternate antennas)
+  const int npilot = p.npilot;          // pilot units per group (the plan uses 1: the epilogue takes den from it)
   const int per_group = npilot + p.dc;  // units per group
   const int ngroups = p.ngroups;
   const int lanes = ngroups * per_group * GI;
@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   const size_t bar_bytes = FC::bar_bytes(lanes, ngroups);
   float2* slots = reinterpret_cast<float2*>(smem_raw + bar_bytes);  // [NSTAGE][lanes][SS]
   float2* ring = slots + (size_t)NSTAGE * lanes * SS;               // [ngroups][RING][GI][HS]
+  float* den_sh = reinterpret_cast<float*>(ring + (size_t)ngroups * RING * GI * HS);  // [ngroups][GI][M]
 
   const int unit = threadIdx.x / UT;
   const int u = threadIdx.x - unit * UT;
@@ -327,43 +328,32 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   }
   const uint32_t t_epi = prof ? sm_clock() : 0u;
 
-  // ---- epilogue: combine the pilots' den partials, divide, demap ----------
+  // ---- epilogue: den from the pilot unit, divide, demap --------------------
+  // The pilot unit publishes den = sum_n |H_n|^2 (its (h.x^2, h.y^2) sums)
+  // into the item's den buffer; ONE barrier then covers the den hand-off,
+  // the end of the ring traffic and the TMEM reads before the dealloc.
   float a[NACC];
   acc_load(a);  // every unit: its accumulators back to registers
+  float* dsh = den_sh + (size_t)(grp * GI + sub) * M;
+  if (is_pilot) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) dsh[i * G + t] = a[2 * i] + a[2 * i + 1];
+  }
   if constexpr (USE_TMEM) tmem_fence_before();
-  __syncthreads();  // ring traffic finished; TMEM reads done
+  __syncthreads();
   if constexpr (USE_TMEM) {
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(*tmem_slot, tmem_cols);
   }
   uint32_t flag = 0;
-  // den partial of pilot unit q lives in ring slot q of this item
-  if (is_pilot) {
-    float* dpart = reinterpret_cast<float*>(hring_grp + (size_t)sl * GI * HS);
-#pragma unroll
-    for (int i = 0; i < P; ++i) dpart[i * G + t] = a[2 * i] + a[2 * i + 1];
-  }
-  __syncthreads();
-  float* dslot = reinterpret_cast<float*>(hring_grp);
-  float den[P];
-  if (sl == 0) {
+  if (is_pilot && active) {
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-      den[i] = dslot[i * G + t];
-      for (int q = 1; q < npilot; ++q) den[i] += reinterpret_cast<const float*>(hring_grp + (size_t)q * GI * HS)[i * G + t];
+      const float dn = a[2 * i] + a[2 * i + 1];
+      if (!isfinite(dn)) flag |= 1u;
+      if (p.mode == 0 && dn < p.eps) flag |= 2u;  // partial sums: erasure is decided after the combine
     }
-  }
-  __syncthreads();
-  if (sl == 0) {
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      dslot[i * G + t] = den[i];
-      if (active) {
-        if (!isfinite(den[i])) flag |= 1u;
-        if (p.mode == 0 && den[i] < p.eps) flag |= 2u;  // partial sums: erasure is decided after the combine
-      }
-    }
-    if (active && chunk == 0) {
+    if (chunk == 0) {
       float* wdst = p.mode == 0 ? p.weights : p.part_den;
       long long wrow = (long long)shard * p.n_frames + f;
       if (p.mode == 1 && p.den_dst != nullptr) {  // routed to the frame's owner
@@ -374,11 +364,11 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
       if (wdst != nullptr) {
         float* w = wdst + wrow * M + t;
 #pragma unroll
-        for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = den[i];
+        for (int i = 0; i < P; ++i) w[shifted_bin<M>(i, 0)] = a[2 * i] + a[2 * i + 1];
       }
     }
   }
-  __syncthreads();
+  float* dslot = dsh;
   if (!is_pilot && active) {
     const long long sym_base = (((long long)shard * p.n_frames + f) * p.n_data + d) * M;
     if (p.mode == 0) {
