@@ -621,12 +621,8 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
 #pragma unroll
         for (int i = 0; i < P; ++i) {
           if (!mine(i)) continue;
-          const float dd = fmaxf(den[i], p.eps);  // np.maximum(den, eps)
-          const float2 shv = make_float2(a[2 * i] / dd, a[2 * i + 1] / dd);
-          if (!isfinite(shv.x) || !isfinite(shv.y)) flag |= 1u;
           const int j = shifted_bin<M>(i, 0);
-          sdst[j] = shv;
-          demap_store(shv, qp, bdst + (long long)j * p.qb);
+          flag |= finish_subcarrier(a[2 * i], a[2 * i + 1], den[i], p.eps, sdst + j, bdst + (long long)j * p.qb, qp);
         }
       } else {
         float2* ndst = p.part_num + sym_base + t;

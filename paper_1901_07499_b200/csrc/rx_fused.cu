@@ -377,12 +377,8 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
       uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        const float dd = fmaxf(dslot[i * G + t], p.eps);  // np.maximum(den, eps)
-        const float2 sh = make_float2(a[2 * i] / dd, a[2 * i + 1] / dd);
-        if (!isfinite(sh.x) || !isfinite(sh.y)) flag |= 1u;
         const int j = shifted_bin<M>(i, 0);
-        sdst[j] = sh;
-        demap_store(sh, q, bdst + (long long)j * p.qb);
+        flag |= finish_subcarrier(a[2 * i], a[2 * i + 1], dslot[i * G + t], p.eps, sdst + j, bdst + (long long)j * p.qb, q);
       }
     } else {
       float2* ndst = p.part_num + sym_base + t;
