@@ -19,6 +19,9 @@ if os.environ.get("OFDMRX_VARIANT_LIB"):  # experiment build (build.py --variant
     _lib.LIB_PATH = os.environ["OFDMRX_VARIANT_LIB"]
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+if cfg_name not in bench.CONFIGS:  # "NxM": N antennas, FFT M, CP M/8, 16-QAM, 10 data symbols
+    n_, m_ = (int(v) for v in cfg_name.split("x"))
+    bench.CONFIGS[cfg_name] = (n_, m_, max(1, m_ // 8), 16, 10, 1024)
 n, m, cp, qam, d, F = bench.CONFIGS[cfg_name]
 if len(sys.argv) > 2:
     F = int(sys.argv[2])
