@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of the M = 128 CTA shape over a few sweep cells (developer tool)
-for c in "4x128 4096" "16x128 4096" "64x128 4096" "128x128 2978"; do
-  bash scripts/ab_variants.sh "$c" base m128x3
+# A/B over the rx_fused shapes (developer tool): usage bash scripts/ab_c2.sh variant...
+for c in "C2 1000" "C2 2000" "16x128 4096" "128x128 2978" "C1 65536"; do
+  bash scripts/ab_variants.sh "$c" "$@"
 done
