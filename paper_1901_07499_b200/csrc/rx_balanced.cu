@@ -615,15 +615,21 @@ __global__ void __launch_bounds__(BMAXW * 32, BalCfg<M>::MIN_CTAS) rx_balanced_k
       }
       const long long sym_base = ((long long)f * D + d_own) * M;
       if (p.mode == 0) {
-        const QamParams qp{p.qb, p.levels, p.qscale};
         float2* sdst = p.s_hat + sym_base + t;
         uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
+#ifdef OFDMRX_EPI_PLAIN
+        const QamParams qp{p.qb, p.levels, p.qscale};
 #pragma unroll
         for (int i = 0; i < P; ++i) {
           if (!mine(i)) continue;
           const int j = shifted_bin<M>(i, 0);
           flag |= finish_subcarrier(a[2 * i], a[2 * i + 1], den[i], p.eps, sdst + j, bdst + (long long)j * p.qb, qp);
         }
+#else
+        flag |= finish_points<P>(
+            a, [&](int i) { return den[i]; }, p.eps, p.qb, p.levels, p.qscale, sdst, bdst,
+            [](int i) { return shifted_bin<M>(i, 0); }, mine);
+#endif
       } else {
         float2* ndst = p.part_num + sym_base + t;
         if (p.num_dst != nullptr) {

@@ -372,14 +372,20 @@ __global__ void __launch_bounds__(PlanInfo<M>::MAX_THREADS, PlanInfo<M>::MIN_CTA
   if (!is_pilot && active) {
     const long long sym_base = (((long long)shard * p.n_frames + f) * p.n_data + d) * M;
     if (p.mode == 0) {
-      const QamParams q{p.qb, p.levels, p.qscale};
       float2* sdst = p.s_hat + sym_base + t;
       uint8_t* bdst = p.bits + (sym_base + t) * p.qb;
+#ifdef OFDMRX_EPI_PLAIN
+      const QamParams q{p.qb, p.levels, p.qscale};
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const int j = shifted_bin<M>(i, 0);
         flag |= finish_subcarrier(a[2 * i], a[2 * i + 1], dslot[i * G + t], p.eps, sdst + j, bdst + (long long)j * p.qb, q);
       }
+#else
+      flag |= finish_points<P>(
+          a, [&](int i) { return dslot[i * G + t]; }, p.eps, p.qb, p.levels, p.qscale, sdst, bdst,
+          [](int i) { return shifted_bin<M>(i, 0); }, [](int) { return true; });
+#endif
     } else {
       float2* ndst = p.part_num + sym_base + t;
       if (p.num_dst != nullptr) {
