@@ -446,6 +446,22 @@ def run_b200(args, cfg_name, world, rank, local):
     oracle_check = (check_vs_oracle(cfg_name, rx_host, s0, out, lo, hi, args.oracle_frames, check_h=sharded is None)
                     if args.oracle_frames else None)
 
+    # one step = one receive_frames call; unless --eager, the call is captured
+    # once in a CUDA graph and replayed, so host-side Python / enqueue jitter
+    # cannot starve short steps (C2: 0.13 ms) inside the device-timed regions
+    launch_mode = "eager"
+    if sharded is None and not args.eager:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            step()
+        stream.wait_stream(cap)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        step = graph.replay  # noqa: F811
+        launch_mode = "cuda_graph"
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
         time.sleep(0.3)  # sampler running before the warm-up
@@ -525,8 +541,11 @@ def run_b200(args, cfg_name, world, rank, local):
                    "frames_per_gpu": F, "global_frames": F if sharded is not None else F * world, "parallelism": (f"antenna-sharded x{world} ({args.exchange} exchange of MRC partials"
                                    f"{' over peer memory, no NCCL' if args.exchange == 'peer' else ' over NCCL'})"
                                    if sharded is not None else f"frame-sharded x{world}"),
-                   "input_bytes_per_gpu": int(x.numel() * 8), "l2": "inputs 6.3 GB/GPU > L2, no flush needed"
-                   if x.numel() * 8 > 126e6 else "inputs smaller than L2"},
+                   "input_bytes_per_gpu": int(x.numel() * 8),
+                   "l2": f"inputs {x.numel() * 8 / 1e9:.2f} GB/GPU > L2 (126 MB), no flush needed"
+                   if x.numel() * 8 > 126e6 else "inputs smaller than L2",
+                   "launch": ("one receive_frames call per step, captured once in a CUDA graph and replayed"
+                              if launch_mode == "cuda_graph" else "one receive / exchange call per step, eager")},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_detail": traffic_detail, "peak_source": peak_kind,
@@ -1025,6 +1044,8 @@ def main():
                     help="second timed region of back-to-back steps (power-cap regime); 0 = off")
     ap.add_argument("--oracle-frames", type=int, default=16,
                     help="distinct frames of the benched launch checked against the CPU oracle; 0 = off")
+    ap.add_argument("--eager", action="store_true",
+                    help="call receive_frames eagerly in the timed loops instead of replaying its CUDA graph")
     ap.add_argument("--no-latency", dest="latency", action="store_false",
                     help="skip the single-frame latency section (C1 and C3)")
     ap.add_argument("--latency-reps", type=int, default=200)

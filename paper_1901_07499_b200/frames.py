@@ -68,14 +68,34 @@ def _pilot_values(pilot, fft_len):
     return vals
 
 
+_DEFAULT_PILOT_INFO = {}  # fft_len -> (values, options) of the default pilot, validated once
+
+
+def _pilot_info(pilot, fft_len):
+    """(values, OFDMRX pilot options, cache key) of a pilot.  The default pilot
+    (pilot=None, waveform.py:214-220) is built and validated once per FFT
+    length -- it dominated the host cost of a receive call; a caller's table
+    is validated on every call (it may have been modified in between)."""
+    if pilot is None:
+        hit = _DEFAULT_PILOT_INFO.get(fft_len)
+        if hit is None:
+            vals = _pilot_values(None, fft_len)
+            hit = _DEFAULT_PILOT_INFO[fft_len] = (vals, device.pilot_options(vals), ("default", fft_len))
+        return hit
+    vals = _pilot_values(pilot, fft_len)
+    return vals, device.pilot_options(vals), None
+
+
 class PilotCache:
-    """Device copies of pilot tables, keyed by (device, values)."""
+    """Device copies of pilot tables, keyed by (device, values) -- or by
+    (device, key) for the default pilots of _pilot_info."""
 
     def __init__(self):
         self._cache = {}
 
-    def get(self, vals, dev):
-        key = (str(dev), vals.shape[0], hash(np.asarray(vals, dtype=np.complex64).tobytes()))
+    def get(self, vals, dev, key=None):
+        key = (str(dev), key) if key is not None else (
+            str(dev), vals.shape[0], hash(np.asarray(vals, dtype=np.complex64).tobytes()))
         t = self._cache.get(key)
         if t is None:
             t = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.complex64)).to(dev)
@@ -133,11 +153,11 @@ def receive_frames(rx, cfg, pilot=None, *, symbol0_offset=0, n_data=None, eps=de
 
 def _launch_rx(desc_args, x, cfg, pilot, out, want_h, zf, check, stream, profile=False, latency=False):
     f, n, _, _, n_data = desc_args[:5]
-    pvals = _pilot_values(pilot, cfg.fft_len)
-    opts = device.pilot_options(pvals) | (_lib.OPT_LATENCY if latency else 0)
+    pvals, popts, pkey = _pilot_info(pilot, cfg.fft_len)
+    opts = popts | (_lib.OPT_LATENCY if latency else 0)
     desc = device.make_desc(*desc_args, options=opts, rx_samples=x.numel())
     device.check_desc(desc)
-    pv = _PILOTS.get(pvals, x.device)
+    pv = _PILOTS.get(pvals, x.device, pkey)
     with device.on_stream(stream):  # outputs allocated / zeroed on the launch stream
         if out is None:
             out = allocate_outputs(f, n, cfg.fft_len, n_data, cfg.qam_order, x.device, want_h=want_h, zf=zf)
