@@ -539,7 +539,7 @@ def run_b200(args, cfg_name, world, rank, local):
                 f"{DISTINCT} distinct frames tiled on device",
         "config": {"workload": f"{cfg_name}: {n} ant x FFT {m} (CP {cp}), {qam}-QAM, 1 pilot + {d} data symbols/frame",
                    "frames_per_gpu": F, "global_frames": F if sharded is not None else F * world, "parallelism": (f"antenna-sharded x{world} ({args.exchange} exchange of MRC partials"
-                                   f"{' over peer memory, no NCCL' if args.exchange == 'peer' else ' over NCCL'})"
+                                   f"{' over peer memory, no NCCL' if args.exchange == 'peer' else ' over ' + _dist_backend_name()})"
                                    if sharded is not None else f"frame-sharded x{world}"),
                    "input_bytes_per_gpu": int(x.numel() * 8),
                    "l2": f"inputs {x.numel() * 8 / 1e9:.2f} GB/GPU > L2 (126 MB), no flush needed"
@@ -650,6 +650,12 @@ def comm_info(world, data_path):
             keep = [ln.strip()[-160:] for ln in fh if "nranks" in ln or "Init COMPLETE" in ln or "NVLS" in ln]
         info["nccl_init_log"] = keep[:4]
     return info
+
+
+def _dist_backend_name():
+    import torch.distributed as dist
+
+    return (dist.get_backend().upper() if dist.is_available() and dist.is_initialized() else "NCCL")
 
 
 def run_latency(args):
